@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark: PARSE rank-expert hot path on B200 (BASELINE.json metric
+"prefill & decode tokens/s, LLaMA-7B SVD@0.6 rank-expert layers, 1-8 B200").
+
+Default workload = BASELINE.json configs[1] ("config2"): LLaMA-7B MLP block
+(gate/up 4096->11008, down 11008->4096) at ratio 0.6 (K=1194, r_store=2388),
+bf16 storage, f32 accumulation, decode batch 1, the expert subset S taken from
+a pattern-cache hit (N=1024 x d=4096 fp64 cache) and reused across every decode
+step.  One step = one decode token through the block: up, gate (rank-expert
+linears over the packed S arena), silu(gate)*up, down.
+
+  value  -- device-resident tokens/s, whole job (sum over ranks), CUDA-graph
+            replay of the step chain, inputs already in HBM; 4 MLP-block weight
+            replicas rotated per step (433 MB packed > 126 MB L2).
+  e2e    -- the same steps through the public API with the per-step input
+            copied H2D from pinned host memory and the result read back D2H
+            inside the timed region.
+  roofline -- the dominant rank-expert linear forward (up-projection: stage-1
+            GEMV + stage-2 GEMV kernels), algorithmic bytes K(m+n)*2 + x + y per
+            launch / CUDA-event time, vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline -- the reference's own CPU path (oracle/_ref: aggregate_layout +
+            aggregated_forward<float>, exec_engine.hpp:113,194) on this host's
+            cores, bounded sample.
+
+--impl reference runs only the reference CPU arm (rank 0) and prints its line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill & decode tokens/s, LLaMA-7B SVD@0.6 rank-expert layers, 1–8 B200"
+D_MODEL, D_FF, RATIO = 4096, 11008, 0.6
+N_CACHE, MIN_SIM, PSI = 1024, 0.80, 0.9
+REPLICAS = 4
+
+
+def shapes():
+    from paper_2605_08568_b200 import single_layer_k, store_rank
+    out = {}
+    for name, (m, n) in {"up": (D_FF, D_MODEL), "gate": (D_FF, D_MODEL), "down": (D_MODEL, D_FF)}.items():
+        K = single_layer_k(m, n, RATIO)
+        out[name] = (m, n, K, store_rank(K, min(m, n)))
+    return out
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- reference CPU arm
+
+def reference_arm(steps: int, warmup: int, threads: int | None = None, target_s: float = 0.0):
+    """The reference's own served path on host cores: ExecEngine<float>'s
+    aggregated_forward over the hit pattern's layout, one decode token = the
+    three MLP linears at T=1.  `threads` independent decode streams."""
+    from oracle import pyoracle
+    kind = "reference" if pyoracle.available("reference") else "port"
+    o = pyoracle.Oracle(kind)
+    threads = threads or os.cpu_count() or 1
+    sh = shapes()
+    rng = np.random.default_rng(0)
+    aggs = {}
+    for name, (m, n, K, r) in sh.items():
+        sig = 1.0 / (1.0 + np.arange(r) / 64.0)
+        A = rng.standard_normal((m, r)) * (sig / np.sqrt(m))
+        B = rng.standard_normal((n, r)) / np.sqrt(n)
+        pat = pyoracle.make_patterns(17171, 1, [(r, K)])[0][0]
+        aggs[name] = o.aggregate_layout(A, B, [pat], PSI, elem=4)
+        del A, B
+    xs = [rng.standard_normal((D_MODEL, 1)).astype(np.float32) for _ in range(threads)]
+
+    def token(i):
+        x = xs[i]
+        u = aggs["up"].forward(0, x)
+        g = aggs["gate"].forward(0, x)
+        act = (g / (1.0 + np.exp(-g)) * u).astype(np.float32)
+        aggs["down"].forward(0, act)
+
+    def run(nsteps):
+        ths = [threading.Thread(target=lambda i=i: [token(i) for _ in range(nsteps)]) for i in range(threads)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return time.perf_counter() - t0
+
+    run(warmup)
+    wall = run(steps)
+    toks = steps * threads
+    return {"value": toks / wall, "unit": "tokens/s", "cores": threads, "kind": kind,
+            "sample": f"{threads} threads x {steps} decode tokens (3 MLP linears, T=1, aggregated_forward<float>)",
+            "ms_per_step": wall / steps * 1e3}
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def build_block(pg, torch, sh, dev, seed):
+    """Random-init rank-expert MLP block in the device layout (B^T expert-major,
+    A [m, r_store]); A columns scaled by sigma_e = 1/(1+e/64)."""
+    g = torch.Generator(device=dev).manual_seed(seed)
+    layers = {}
+    for name, (m, n, K, r) in sh.items():
+        bt = (torch.randn((r, n), generator=g, device=dev) / n ** 0.5).to(torch.bfloat16)
+        sig = 1.0 / (1.0 + torch.arange(r, device=dev, dtype=torch.float32) / 64.0)
+        a = (torch.randn((m, r), generator=g, device=dev) * sig / m ** 0.5).to(torch.bfloat16)
+        layers[name] = pg.FactorizedLayer.from_device(bt, a, K, layer_id=name)
+    return layers
+
+
+def gpu_arm(args, rank, world, local_rank):
+    import torch
+    import paper_2605_08568_b200 as pg
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sh = shapes()
+    hbm_peak, _, peak_kind = peaks()
+
+    # ---- pattern cache: N entries, each with a SelectionMap for the 3 linears
+    pats = pg.make_patterns(17171 + rank, N_CACHE, [(sh[k][3], sh[k][2]) for k in ("up", "gate", "down")])
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    emb = torch.randn((N_CACHE, D_MODEL), generator=gen, device=dev, dtype=torch.float64)
+    emb /= emb.norm(dim=1, keepdim=True)
+    cache = pg.PatternCache(D_MODEL, N_CACHE, MIN_SIM)
+    cache.load([pg.CacheEntry(pg.PromptEmbedding(e), {"up": p[0], "gate": p[1], "down": p[2]})
+                for e, p in zip(emb.cpu().numpy(), pats)])
+    q = emb[7] + 0.05 * torch.randn(D_MODEL, generator=gen, device=dev, dtype=torch.float64)
+    q /= q.norm()
+
+    blocks = [build_block(pg, torch, sh, dev, 100 * rank + j) for j in range(REPLICAS)]
+    torch.cuda.synchronize()
+
+    # ---- prompt-level work (once per prompt): retrieve -> pack the hit's experts
+    t0 = time.perf_counter()
+    res = pg.retrieve(cache, q)
+    assert res.hit and res.entry == 7, (res.entry, res.similarity)
+    aggs = [{k: pg.aggregate_layout(b[k], [res.pattern[k]], PSI) for k in b} for b in blocks]
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t0) * 1e3
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(10):
+        pg.retrieve_device(cache, q)
+    ev1.record()
+    torch.cuda.synchronize()
+    retrieve_us = ev0.elapsed_time(ev1) / 10 * 1e3
+
+    # ---- per-step buffers
+    G = 64  # steps per captured graph
+    xs = torch.randn((G, D_MODEL), generator=gen, device=dev).to(torch.bfloat16)
+    up = torch.empty((G, D_FF), device=dev)
+    gt = torch.empty((G, D_FF), device=dev)
+    act = torch.empty((G, D_FF), device=dev, dtype=torch.bfloat16)
+    y = torch.empty((G, D_MODEL), device=dev)
+    x_host = torch.empty((G, D_MODEL), dtype=torch.bfloat16).pin_memory()
+    x_host.copy_(xs.cpu())
+    y_host = torch.empty((G, D_MODEL), dtype=torch.float32).pin_memory()
+
+    def step(i, host_io):
+        a = aggs[i % REPLICAS]
+        if host_io:
+            xs[i].copy_(x_host[i], non_blocking=True)
+        pg.aggregated_forward(a["up"], 0, xs[i], out=up[i])
+        pg.aggregated_forward(a["gate"], 0, xs[i], out=gt[i])
+        pg.silu_mul(gt[i], up[i], out=act[i])
+        pg.aggregated_forward(a["down"], 0, act[i], out=y[i])
+        if host_io:
+            y_host[i].copy_(y[i], non_blocking=True)
+
+    stream = torch.cuda.Stream(device=dev)
+    graphs = {}
+    for host_io in (False, True):
+        with torch.cuda.stream(stream):
+            for i in range(G):  # warm (kernel attributes, pools) outside capture
+                step(i, host_io)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = pg.launch_count()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(G):
+                step(i, host_io)
+        graphs[host_io] = (g, pg.launch_count() - n0)
+    torch.cuda.synchronize()
+
+    def timed(host_io, steps):
+        g, _ = graphs[host_io]
+        reps = max(1, steps // G)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, args.warmup // G + 1)):
+                g.replay()
+        stream.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            s0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            s1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ms = s0.elapsed_time(s1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, reps * G
+
+    with ClockSampler(local_rank) as clk:
+        ms, nsteps = timed(False, args.steps)
+    ms_e2e, nsteps_e2e = timed(True, args.steps)
+    launches_per_step = graphs[False][1] / G
+
+    # ---- roofline: the up-projection forward, CUDA events on its stream
+    m, n, K, r = sh["up"]
+    alg_bytes = K * (m + n) * 2 + n * 2 + m * 4
+    reps = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for i in range(8):
+            pg.aggregated_forward(aggs[i % REPLICAS]["up"], 0, xs[i], out=up[i])
+        e0.record(stream)
+        for i in range(reps):
+            pg.aggregated_forward(aggs[i % REPLICAS]["up"], 0, xs[i % G], out=up[i % G])
+        e1.record(stream)
+    torch.cuda.synchronize()
+    lin_us = e0.elapsed_time(e1) / reps * 1e3
+    achieved = alg_bytes / (lin_us * 1e-6) / 1e9
+
+    step_bytes = sum(K_ * (m_ + n_) * 2 for (m_, n_, K_, _) in sh.values())
+    tok_s = nsteps / (ms * 1e-3) * world
+    out = {
+        "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": nsteps,
+        "warmup": args.warmup, "ms_per_step": ms / nsteps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init rank-expert factors, seeded)",
+        "config": {"workload": "config2: LLaMA-7B MLP block (gate/up 4096->11008, down 11008->4096) ratio 0.6 "
+                               "K=1194 r_store=2388, decode batch 1, S from a pattern-cache hit reused across steps",
+                   "cache": f"N={N_CACHE} x d={D_MODEL} f64, min_similarity {MIN_SIM}, hit entry {res.entry}",
+                   "l2": f"{REPLICAS} MLP-block weight replicas rotated per step "
+                         f"({REPLICAS * step_bytes / 1e6:.0f} MB packed > 126 MB L2)",
+                   "parallelism": f"dp{world} (independent decode streams per GPU)",
+                   "psi": PSI, "graph": f"CUDA graph of {G} steps replayed"},
+        "e2e": {"value": nsteps_e2e / (ms_e2e * 1e-3) * world, "unit": "tokens/s",
+                "h2d_bytes_per_step": D_MODEL * 2, "d2h_bytes_per_step": D_MODEL * 4},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "up-projection forward (k_stage1_gemv + k_stage2_gemv, 2 launches)",
+                     "alg_bytes_per_launch": alg_bytes, "avg_us": lin_us, "peak_kind": peak_kind},
+        "step_roofline": {"alg_bytes_per_step": step_bytes,
+                          "achieved_GBps": step_bytes / (ms / nsteps * 1e-3) / 1e9,
+                          "frac": step_bytes / (ms / nsteps * 1e-3) / 1e9 / hbm_peak},
+        "gpu_launches": int(launches_per_step * nsteps),
+        "clocks": clk.summary(),
+        "prefill_setup": {"retrieve_us": retrieve_us, "retrieve_plus_pack_ms_host": setup_ms},
+    }
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        st = max(1, min(args.steps, 20))
+        ref = reference_arm(st, max(1, min(args.warmup, 1)))
+        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": 0, "steps": st,
+                "warmup": max(1, min(args.warmup, 1)), "ms_per_step": ref["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "impl": "reference",
+                "config": {"workload": "config2: LLaMA-7B MLP block decode batch 1 (reference CPU "
+                                       "aggregated_forward<float>, exec_engine.hpp:194)"},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = gpu_arm(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1:
+            ref = reference_arm(args.cpu_steps, 1)
+            out["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

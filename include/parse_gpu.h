@@ -1,0 +1,224 @@
+/*
+ * parse_gpu.h -- C-ABI of the B200 (sm_100a) rank-expert hot path.
+ *
+ * Drop-in boundary for the reference's C++ operator surface
+ * (/root/reference/proj/include/parse/*.hpp).  Plain pointers and sizes, no
+ * torch types.  Every entry point cites the reference interface it replaces.
+ * The C++ mirror that keeps the reference signatures intact is
+ * include/parse_gpu.hpp (namespace parse::gpu); the Python mirror is the
+ * paper_2605_08568_b200 package.
+ *
+ * Conventions
+ *  - Return value: PG_OK or an error class mirroring the reference's exception
+ *    types (std::invalid_argument / std::out_of_range / std::runtime_error), plus
+ *    PG_CUDA_ERROR.  pg_last_error() returns a thread-local message (the
+ *    reference's exception text where one exists, e.g. "select_topk: K out of
+ *    range").
+ *  - "dev" pointers are device memory; "host" pointers are host memory.
+ *  - Calls taking a pg_stream are asynchronous on that stream (cudaStream_t, 0 =
+ *    legacy default).  Device buffers passed in are borrowed until the stream
+ *    is synchronised.  Calls that return host values synchronise the stream.
+ *  - Layouts: PG_FEATURE_MAJOR is the reference's Mat layout for activations
+ *    (X is n x T row-major, toy_lm.hpp:110); PG_TOKEN_MAJOR is T x n.  For
+ *    T == 1 they are the same bytes.
+ *  - Handles are immutable after creation (concurrent readers
+ *    allowed); the library is thread-safe for distinct streams.
+ */
+#ifndef PARSE_GPU_H
+#define PARSE_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_OK 0
+#define PG_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define PG_OUT_OF_RANGE 2     /* std::out_of_range */
+#define PG_RUNTIME_ERROR 3    /* std::runtime_error */
+#define PG_CUDA_ERROR 4
+
+typedef enum { PG_F64 = 0, PG_F32 = 1, PG_BF16 = 2 } pg_dtype;
+typedef enum { PG_FEATURE_MAJOR = 0, PG_TOKEN_MAJOR = 1 } pg_layout;
+typedef void* pg_stream; /* cudaStream_t */
+
+typedef struct pg_router_s* pg_router; /* RouterParams (router.hpp:15-20) on device   */
+typedef struct pg_layer_s* pg_layer;   /* FactorizedLayer (factorize.hpp:28-37)       */
+typedef struct pg_agg_s* pg_agg;       /* AggregatedLayer<T> (exec_engine.hpp:97-110) */
+typedef struct pg_cache_s* pg_cache;   /* PatternCache embeddings (pattern_cache.hpp:31-36) */
+
+const char* pg_last_error(void);
+int pg_abi_version(void);
+/* Number of this library's kernels launched so far on this host thread's process
+ * (monotone counter; bench.py reports deltas as gpu_launches). */
+uint64_t pg_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* a5-a7: routing  (router.hpp:41-61,80-88)                            */
+/* ------------------------------------------------------------------ */
+
+/* mean_pool (router.hpp:80-88), bit-exact: h[p*n+i] = (sequential sum over the
+ * prompt's tokens of x(i,t)) / T_p.  x dtype f64/f32/bf16 (widened exactly to
+ * f64).  offsets_host[P+1] are token offsets of each prompt into x
+ * (P=1, offsets {0,T} for one sequence).  h_dev: P x n f64. */
+int pg_mean_pool(const void* x_dev, pg_dtype x_dtype, pg_layout layout, size_t n,
+                 const int64_t* offsets_host, size_t n_prompts, double* h_dev, pg_stream stream);
+
+/* score (router.hpp:41-46): z = theta*h + bias.  exact=1 reproduces the
+ * reference's sequential dot bit-for-bit; exact=0 is the fast warp-tree GEMV
+ * (|z - z_ref| <= 4(n+2)u(sum|theta_ij h_j| + |b_i|), u = 2^-53). */
+int pg_router_create(pg_router* out, size_t r, size_t n, const double* theta_host,
+                     const double* bias_host);
+/* theta_dev r x n and bias_dev r (f64) already on device; copy=0 borrows them. */
+int pg_router_create_device(pg_router* out, size_t r, size_t n, const double* theta_dev,
+                            const double* bias_dev, int copy);
+int pg_router_destroy(pg_router r);
+int pg_score(pg_router router, const double* h_dev, size_t n_prompts, double* logits_dev,
+             int exact, pg_stream stream);
+
+/* select_topk (router.hpp:49-61) on given logits: K largest, ties toward the
+ * lower index, output ascending.  Exact (pure comparisons). */
+int pg_select_topk(const double* logits_dev, size_t r, size_t n_prompts, size_t k,
+                   uint32_t* sel_dev, pg_stream stream);
+
+/* Fused RoutingProvider::apply routing step (model.hpp:100-104):
+ * select_topk(score(theta, mean_pool(x)), K) per prompt, bit-identical to the
+ * reference (fast GEMV + error-bounded band + reference-order recompute of the
+ * rows that straddle the K-th logit).  sel_dev: n_prompts x K ascending u32.
+ * logits_dev (nullable, n_prompts x r) receives the logits used for selection. */
+int pg_route_select(pg_router router, const void* x_dev, pg_dtype x_dtype, pg_layout layout,
+                    const int64_t* offsets_host, size_t n_prompts, size_t k, uint32_t* sel_dev,
+                    double* logits_dev, pg_stream stream);
+
+/* ------------------------------------------------------------------ */
+/* a9-a12: pattern cache  (pattern_cache.hpp:38-65,95-124)             */
+/* ------------------------------------------------------------------ */
+
+typedef struct {
+    size_t entry;      /* RetrieveResult::entry      */
+    double similarity; /* RetrieveResult::similarity */
+    int hit;           /* RetrieveResult::hit        */
+    int exact_similarity; /* 1 if similarity is the reference-order value */
+} pg_retrieve_result;
+
+/* cosine (pattern_cache.hpp:38-47), reference order, bit-exact. out_dev: 1 f64 */
+int pg_cosine(const double* a_dev, const double* b_dev, size_t d, double* out_dev,
+              pg_stream stream);
+int pg_cache_create(pg_cache* out, size_t d, size_t capacity, double min_similarity);
+int pg_cache_destroy(pg_cache c);
+int pg_cache_size(pg_cache c, size_t* size_out);
+/* cache_insert (pattern_cache.hpp:120-124): append iff size < capacity.
+ * emb: d f64 (host or device per emb_on_device).  *inserted = 0 when full. */
+int pg_cache_insert(pg_cache c, const double* emb, int emb_on_device, int* inserted,
+                    pg_stream stream);
+/* Bulk load of N x d embeddings (load_cache, pattern_cache.hpp:294-327). */
+int pg_cache_load(pg_cache c, const double* emb_host, size_t n_entries);
+/* retrieve (pattern_cache.hpp:104-117): exhaustive cosine scan, first maximum,
+ * hit = sim >= min_similarity.  entry/hit bit-exact vs the reference; the
+ * similarity is the reference-order value when exact_similarity=1 (or when the
+ * guard had to recompute it), else within 4(d+4)u(...)-relative.
+ * query_dev: d f64.  result_host (nullable) synchronises the stream;
+ * entry_dev (nullable, int32) / hit_dev (nullable, int32) stay on device so a
+ * forward can consume the hit without a host round trip. */
+int pg_retrieve(pg_cache c, const double* query_dev, int exact_similarity,
+                pg_retrieve_result* result_host, int32_t* entry_dev, int32_t* hit_dev,
+                pg_stream stream);
+/* embed_prompt's pooling half (pattern_cache.hpp:60-64): mean_pool of the
+ * block-0 output (d x T) then divide by vec_norm; bit-exact.  Degenerate
+ * (norm < 1e-12) -> PG_RUNTIME_ERROR "degenerate embedding" (synchronises). */
+int pg_embed_normalize(const void* x_dev, pg_dtype x_dtype, pg_layout layout, size_t d,
+                       size_t T, double* emb_dev, pg_stream stream);
+
+/* ------------------------------------------------------------------ */
+/* a2, a13, a16: factorized layer + value path (rank_experts.hpp:52-72) */
+/* ------------------------------------------------------------------ */
+
+/* Upload a FactorizedLayer: A m x r_store, B n x r_store (host f64, the
+ * reference's Matd layout, factorize.hpp:32-33).  Stored on device as
+ * expert-major B^T [r_store x n] and A [m x r_store] in `storage`. */
+int pg_layer_create(pg_layer* out, size_t m, size_t n, size_t r_store, size_t K,
+                    const double* A_host, const double* B_host, pg_dtype storage);
+/* Device factors already in the device layout (bt_dev r_store x n, a_dev
+ * m x r_store, both `storage` dtype); copy=0 borrows them. */
+int pg_layer_create_device(pg_layer* out, size_t m, size_t n, size_t r_store, size_t K,
+                           const void* bt_dev, const void* a_dev, pg_dtype storage, int copy);
+int pg_layer_destroy(pg_layer l);
+int pg_layer_info(pg_layer l, size_t* m, size_t* n, size_t* r_store, size_t* K,
+                  pg_dtype* storage);
+
+/* check_selection (rank_experts.hpp:30-37) on a host selection. */
+int pg_check_selection(pg_layer l, const uint32_t* sel_host, size_t k);
+
+/* masked_forward (rank_experts.hpp:52-72) == scattered_forward
+ * (exec_engine.hpp:239-252): y = sum_{e in S} A[:,e] (B[:,e]^T x), fp32
+ * accumulation (f64 for f64 storage).  x dtype == storage; y dtype is
+ * storage or PG_F32.  sel is host (validated, uploaded) when sel_on_device=0,
+ * else a device array trusted to be valid (e.g. pg_route_select output). */
+int pg_masked_forward(pg_layer l, const uint32_t* sel, size_t k, int sel_on_device,
+                      const void* x_dev, pg_layout layout, size_t T, void* y_dev,
+                      pg_dtype y_dtype, pg_stream stream);
+
+/* ------------------------------------------------------------------ */
+/* a14-a15, a19: aggregated layout (exec_engine.hpp:97-236)             */
+/* ------------------------------------------------------------------ */
+
+/* aggregate_layout<T> (exec_engine.hpp:112-164) built on device by gather:
+ * shared experts (freq >= psi*P) at the arena head, each pattern's residual
+ * experts in its own block.  patterns_host: concatenated ids, ks_host[P]. */
+int pg_aggregate_layout(pg_agg* out, pg_layer l, const uint32_t* patterns_host,
+                        const size_t* ks_host, size_t n_patterns, double psi, pg_stream stream);
+int pg_agg_destroy(pg_agg g);
+int pg_agg_patterns(pg_agg g, size_t* n_patterns);
+int pg_agg_shared(pg_agg g, size_t* count, uint32_t* ids_host /* nullable */);
+/* residual ids (ascending), the reference's arena_offset, use_shared flags */
+int pg_agg_residual(pg_agg g, size_t pattern, size_t* count, uint32_t* ids_host,
+                    size_t* arena_offset, uint8_t* use_shared_host);
+/* AccessTrace (exec_engine.hpp:90-92): arena columns one forward touches, in
+ * the reference's column numbering; *count then cols_host (nullable). */
+int pg_agg_trace(pg_agg g, size_t pattern, size_t* count, size_t* cols_host);
+/* Device bytes of the arena (storage_overhead accounting, :310-318). */
+int pg_agg_bytes(pg_agg g, size_t* bytes);
+
+/* aggregated_forward<T> (exec_engine.hpp:193-236) for one pattern.
+ * pattern_dev (nullable int32 on device) overrides `pattern` without a host
+ * round trip (e.g. the entry index written by pg_retrieve). */
+int pg_aggregated_forward(pg_agg g, size_t pattern, const int32_t* pattern_dev,
+                          const void* x_dev, pg_layout layout, size_t T, void* y_dev,
+                          pg_dtype y_dtype, pg_stream stream);
+
+/* Heterogeneous batch (prefill or decode): prompt p owns tokens
+ * [offsets_host[p], offsets_host[p+1]) of token-major x and is served with
+ * pattern patterns_host[p] of the aggregated layout.  y token-major. */
+int pg_aggregated_forward_batched(pg_agg g, const int32_t* patterns_host,
+                                  const int64_t* offsets_host, size_t n_prompts,
+                                  const void* x_dev, void* y_dev, pg_dtype y_dtype,
+                                  pg_stream stream);
+
+/* MLP glue between upgate() and down_proj() (toy_lm.hpp:250-257):
+ * act[i] = silu(gate[i]) * up[i], computed in f32 (f64 for f64 inputs) and
+ * stored in act_dtype.  gate/up dtype in_dtype (PG_F32 or PG_F64). */
+int pg_silu_mul(const void* gate_dev, const void* up_dev, pg_dtype in_dtype, size_t count,
+                void* act_dev, pg_dtype act_dtype, pg_stream stream);
+
+/* ------------------------------------------------------------------ */
+/* host utilities                                                      */
+/* ------------------------------------------------------------------ */
+
+/* Rng (rng.hpp:10-41): count gaussians from Rng(seed) -- bit-identical to the
+ * reference's fixtures. */
+void pg_rng_fill_gaussian(uint64_t seed, double* out_host, size_t count);
+/* The reference's prefix-biased pattern generator (test_acceptance.cpp:412-425)
+ * in O(K log r) per draw: same ids as the reference's O(K r) vector::erase. */
+void pg_make_patterns(uint64_t seed, size_t n_patterns, const size_t* r_stores,
+                      const size_t* ks, size_t n_layers, uint32_t* out_host);
+/* Device-side synthetic fill (bench weights too large for host f64):
+ * out[i] = scale * N(0,1) from a counter-based hash of (seed, i). */
+int pg_fill_normal_device(void* out_dev, pg_dtype dtype, size_t count, uint64_t seed,
+                          double scale, pg_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,761 @@
+// capi.cu -- the extern "C" boundary (include/parse_gpu.h): handles, argument
+// validation with the reference's exception classes/messages, workspace, and
+// dispatch to the sm_100a kernels.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_err;
+void set_error(int code, const std::string& msg) {
+    (void)code;
+    t_err = msg;
+}
+
+// ---- kernel launchers (route.cu, cache.cu, values.cu, umma.cu) ----
+void launch_mean_pool(const void* x, pg_dtype dt, pg_layout lay, int n, int64_t ttot,
+                      const int64_t* offs_dev, int P, double* h, cudaStream_t st);
+void launch_score(const double* theta, const double* bias, int r, int n, const double* h, int P,
+                  double* z, double* bnd, int exact, cudaStream_t st);
+void launch_select_topk(const double* logits, int r, int P, int K, uint32_t* sel, cudaStream_t st);
+void launch_route_select(const double* zfast, const double* bnd, const double* theta,
+                         const double* bias, const double* h, int r, int n, int K, int P,
+                         uint32_t* sel, double* logits_out, int* stats, cudaStream_t st);
+int max_select_rows();
+void launch_cosine_scan(const double* emb, const double* q, int N, int d, double* sim, double* bnd,
+                        cudaStream_t st);
+void launch_retrieve_select(const double* sim, const double* bnd, const double* emb,
+                            const double* q, int N, int d, double min_sim, int exact_similarity,
+                            double* out_f64, int32_t* out_i32, int32_t* entry_dev,
+                            int32_t* hit_dev, cudaStream_t st);
+void launch_cosine_exact(const double* a, const double* b, int d, double* out, cudaStream_t st);
+void launch_embed_finish(double* h, int d, int* flag, cudaStream_t st);
+int max_cache_dim();
+void launch_gather_rows(pg_dtype dt, const void* src, int64_t lds, const int32_t* idx, int cnt,
+                        int cnt_pad, int cols, void* dst, int64_t ldd, cudaStream_t st);
+void launch_gather_cols(pg_dtype dt, const void* src, int64_t lds, const int32_t* idx, int cnt,
+                        int cnt_pad, int m, void* dst, int64_t ldd, cudaStream_t st);
+int decode_tmax(int T);
+size_t decode_smem_need(pg_dtype wdt, int n, int nslots, int T);
+void launch_decode(pg_dtype wdt, const void* bt, int64_t ldb, const void* a, int64_t lda, SlotMap sm,
+                   int n, int m, const void* x, int fm, int T, void* z, void* y, pg_dtype ydt,
+                   cudaStream_t st);
+size_t simt_ws_elems(int n, int m, int ns, int T);
+void launch_simt(pg_dtype wdt, const void* bt, int64_t ldb, const void* a, int64_t lda, SlotMap sm,
+                 int n, int m, const void* x, int fm, int T, void* ws, void* y, pg_dtype ydt,
+                 cudaStream_t st);
+void launch_fill_normal(void* out, pg_dtype dt, size_t count, uint64_t seed, double scale,
+                        cudaStream_t st);
+void launch_silu_mul(const void* g, const void* u, pg_dtype in_dt, size_t count, void* act,
+                     pg_dtype act_dt, cudaStream_t st);
+
+// ---- stream-ordered scratch (freed when the scope ends, after queued work) ----
+static void init_pool() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t st;
+    Scratch(size_t bytes, cudaStream_t s) : st(s) {
+        init_pool();
+        if (bytes) PG_CUDA_THROW(cudaMallocAsync(&p, (bytes + 255) / 256 * 256, st));
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+};
+
+static void* dev_alloc(size_t bytes) {
+    void* p = nullptr;
+    PG_CUDA_THROW(cudaMalloc(&p, bytes ? bytes : 16));
+    return p;
+}
+
+static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+constexpr int kSlotAlign = 32;  // slot runs aligned to the GEMM K-block / 16 B vectors
+
+// host f64 -> device dtype conversion (round to nearest even for bf16/f32)
+static uint16_t f32_to_bf16_bits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);  // NaN
+    const uint32_t lsb = (u >> 16) & 1u;
+    u += 0x7fffu + lsb;
+    return (uint16_t)(u >> 16);
+}
+static void convert_store(const double* src, size_t count, pg_dtype dt, void* dst) {
+    if (dt == PG_F64) std::memcpy(dst, src, count * 8);
+    else if (dt == PG_F32)
+        for (size_t i = 0; i < count; ++i) static_cast<float*>(dst)[i] = (float)src[i];
+    else
+        for (size_t i = 0; i < count; ++i)
+            static_cast<uint16_t*>(dst)[i] = f32_to_bf16_bits((float)src[i]);
+}
+
+}  // namespace pg
+
+using namespace pg;
+
+// ---------------------------------------------------------------- handles
+struct pg_router_s {
+    int r, n;
+    double* theta;
+    double* bias;
+    bool owned;
+};
+struct pg_layer_s {
+    int m, n, r, K;
+    pg_dtype dt;
+    void* bt;     // [r, ldb]
+    int64_t ldb;  // >= n, 16-byte multiple
+    void* a;      // [m, lda]
+    int64_t lda;  // >= r, 16-byte multiple
+    bool owned;
+};
+struct pg_agg_s {
+    pg_layer layer;
+    int m, n, P;
+    pg_dtype dt;
+    // reference-numbered structure (exec_engine.hpp:97-110)
+    std::vector<uint32_t> shared_ids;
+    std::vector<std::vector<uint32_t>> res_ids;
+    std::vector<std::vector<uint8_t>> use_shared;
+    std::vector<size_t> ref_offset;
+    // device arena: slot runs aligned to kSlotAlign
+    int s_pad;
+    std::vector<int> dev_off, cnt_pad;
+    int arena_cols;
+    void* bt_arena;  // [arena_cols, ldb]
+    int64_t ldb;
+    void* a_arena;   // [m, lda] lda = arena_cols
+    int64_t lda;
+    uint8_t* masks;   // [P, s_pad]
+    int32_t* table;   // [P, 2] (run1_start, run1_len)
+    size_t bytes;
+};
+struct pg_cache_s {
+    int d;
+    size_t capacity, size;
+    double min_sim;
+    double* emb;
+    double* sim;
+    double* bnd;
+    double* out_f64;
+    int32_t* out_i32;
+    int* flag;
+    double* pinned_f64;
+    int32_t* pinned_i32;
+};
+
+#define PG_API_BEGIN try {
+#define PG_API_END                                                \
+    return PG_OK;                                                 \
+    }                                                             \
+    catch (const ::pg::Error& e) {                                \
+        ::pg::set_error(e.code, e.msg);                           \
+        return e.code;                                            \
+    }                                                             \
+    catch (const std::bad_alloc&) {                               \
+        ::pg::set_error(PG_RUNTIME_ERROR, "host allocation failed"); \
+        return PG_RUNTIME_ERROR;                                  \
+    }
+
+static void require(bool ok, int code, const char* msg) {
+    if (!ok) throw Error{code, msg};
+}
+
+extern "C" {
+
+const char* pg_last_error(void) { return t_err.c_str(); }
+int pg_abi_version(void) { return 1; }
+uint64_t pg_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------ routing
+int pg_mean_pool(const void* x, pg_dtype dt, pg_layout lay, size_t n, const int64_t* offs,
+                 size_t P, double* h, pg_stream s) {
+    PG_API_BEGIN
+    require(x && h && offs && P > 0 && n > 0, PG_INVALID_ARGUMENT, "mean_pool: bad arguments");
+    const cudaStream_t st = as_stream(s);
+    Scratch od((P + 1) * 8, st);
+    PG_CUDA_THROW(cudaMemcpyAsync(od.p, offs, (P + 1) * 8, cudaMemcpyHostToDevice, st));
+    launch_mean_pool(x, dt, lay, (int)n, offs[P], od.as<int64_t>(), (int)P, h, st);
+    PG_API_END
+}
+
+int pg_router_create(pg_router* out, size_t r, size_t n, const double* theta, const double* bias) {
+    PG_API_BEGIN
+    require(out && theta && bias && r > 0 && n > 0, PG_INVALID_ARGUMENT, "router: bad arguments");
+    auto* R = new pg_router_s{(int)r, (int)n, nullptr, nullptr, true};
+    R->theta = static_cast<double*>(dev_alloc(r * n * 8));
+    R->bias = static_cast<double*>(dev_alloc(r * 8));
+    PG_CUDA_THROW(cudaMemcpy(R->theta, theta, r * n * 8, cudaMemcpyHostToDevice));
+    PG_CUDA_THROW(cudaMemcpy(R->bias, bias, r * 8, cudaMemcpyHostToDevice));
+    *out = R;
+    PG_API_END
+}
+
+int pg_router_create_device(pg_router* out, size_t r, size_t n, const double* theta,
+                            const double* bias, int copy) {
+    PG_API_BEGIN
+    require(out && theta && bias && r > 0 && n > 0, PG_INVALID_ARGUMENT, "router: bad arguments");
+    auto* R = new pg_router_s{(int)r, (int)n, const_cast<double*>(theta), const_cast<double*>(bias), false};
+    if (copy) {
+        R->theta = static_cast<double*>(dev_alloc(r * n * 8));
+        R->bias = static_cast<double*>(dev_alloc(r * 8));
+        PG_CUDA_THROW(cudaMemcpy(R->theta, theta, r * n * 8, cudaMemcpyDeviceToDevice));
+        PG_CUDA_THROW(cudaMemcpy(R->bias, bias, r * 8, cudaMemcpyDeviceToDevice));
+        R->owned = true;
+    }
+    *out = R;
+    PG_API_END
+}
+
+int pg_router_destroy(pg_router R) {
+    PG_API_BEGIN
+    if (!R) return PG_OK;
+    if (R->owned) {
+        cudaFree(R->theta);
+        cudaFree(R->bias);
+    }
+    delete R;
+    PG_API_END
+}
+
+int pg_score(pg_router R, const double* h, size_t P, double* logits, int exact, pg_stream s) {
+    PG_API_BEGIN
+    require(R && h && logits && P > 0, PG_INVALID_ARGUMENT, "score: bad input length");
+    launch_score(R->theta, R->bias, R->r, R->n, h, (int)P, logits, nullptr, exact ? 1 : 0,
+                 as_stream(s));
+    PG_API_END
+}
+
+int pg_select_topk(const double* logits, size_t r, size_t P, size_t k, uint32_t* sel, pg_stream s) {
+    PG_API_BEGIN
+    require(k != 0 && k <= r, PG_INVALID_ARGUMENT, "select_topk: K out of range");
+    require(logits && sel && P > 0, PG_INVALID_ARGUMENT, "select_topk: bad arguments");
+    require((int)r <= max_select_rows(), PG_INVALID_ARGUMENT, "select_topk: too many experts for device top-k");
+    launch_select_topk(logits, (int)r, (int)P, (int)k, sel, as_stream(s));
+    PG_API_END
+}
+
+int pg_route_select(pg_router R, const void* x, pg_dtype dt, pg_layout lay, const int64_t* offs,
+                    size_t P, size_t k, uint32_t* sel, double* logits_out, pg_stream s) {
+    PG_API_BEGIN
+    require(R && x && offs && sel && P > 0, PG_INVALID_ARGUMENT, "route_select: bad arguments");
+    require(k != 0 && k <= (size_t)R->r, PG_INVALID_ARGUMENT, "select_topk: K out of range");
+    require(R->r <= max_select_rows(), PG_INVALID_ARGUMENT, "select_topk: too many experts for device top-k");
+    const cudaStream_t st = as_stream(s);
+    const size_t r = R->r, n = R->n;
+    Scratch ws((P + 1) * 8 + P * n * 8 + 2 * P * r * 8, st);
+    int64_t* od = ws.as<int64_t>();
+    double* h = reinterpret_cast<double*>(od + P + 1);
+    double* z = h + P * n;
+    double* bnd = z + P * r;
+    PG_CUDA_THROW(cudaMemcpyAsync(od, offs, (P + 1) * 8, cudaMemcpyHostToDevice, st));
+    launch_mean_pool(x, dt, lay, (int)n, offs[P], od, (int)P, h, st);
+    launch_score(R->theta, R->bias, (int)r, (int)n, h, (int)P, z, bnd, 0, st);
+    launch_route_select(z, bnd, R->theta, R->bias, h, (int)r, (int)n, (int)k, (int)P, sel,
+                        logits_out, nullptr, st);
+    PG_API_END
+}
+
+// ------------------------------------------------------------ cache
+int pg_cosine(const double* a, const double* b, size_t d, double* out, pg_stream s) {
+    PG_API_BEGIN
+    require(a && b && out && d > 0, PG_INVALID_ARGUMENT, "cosine: length mismatch");
+    launch_cosine_exact(a, b, (int)d, out, as_stream(s));
+    PG_API_END
+}
+
+int pg_cache_create(pg_cache* out, size_t d, size_t capacity, double min_sim) {
+    PG_API_BEGIN
+    require(out && d > 0, PG_INVALID_ARGUMENT, "cache: bad arguments");
+    require((int)d <= max_cache_dim(), PG_INVALID_ARGUMENT, "cache: d_model too large");
+    auto* c = new pg_cache_s{};
+    c->d = (int)d;
+    c->capacity = capacity;
+    c->size = 0;
+    c->min_sim = min_sim;
+    const size_t cap = std::max<size_t>(capacity, 1);
+    c->emb = static_cast<double*>(dev_alloc(cap * d * 8));
+    c->sim = static_cast<double*>(dev_alloc(cap * 8));
+    c->bnd = static_cast<double*>(dev_alloc(cap * 8));
+    c->out_f64 = static_cast<double*>(dev_alloc(16));
+    c->out_i32 = static_cast<int32_t*>(dev_alloc(16));
+    c->flag = static_cast<int*>(dev_alloc(16));
+    PG_CUDA_THROW(cudaMallocHost(&c->pinned_f64, 16));
+    PG_CUDA_THROW(cudaMallocHost(&c->pinned_i32, 16));
+    *out = c;
+    PG_API_END
+}
+
+int pg_cache_destroy(pg_cache c) {
+    PG_API_BEGIN
+    if (!c) return PG_OK;
+    cudaFree(c->emb); cudaFree(c->sim); cudaFree(c->bnd);
+    cudaFree(c->out_f64); cudaFree(c->out_i32); cudaFree(c->flag);
+    cudaFreeHost(c->pinned_f64); cudaFreeHost(c->pinned_i32);
+    delete c;
+    PG_API_END
+}
+
+int pg_cache_size(pg_cache c, size_t* out) {
+    PG_API_BEGIN
+    require(c && out, PG_INVALID_ARGUMENT, "cache: bad arguments");
+    *out = c->size;
+    PG_API_END
+}
+
+int pg_cache_insert(pg_cache c, const double* emb, int on_dev, int* inserted, pg_stream s) {
+    PG_API_BEGIN
+    require(c && emb, PG_INVALID_ARGUMENT, "cache_insert: bad arguments");
+    if (c->size >= c->capacity) {  // pattern_cache.hpp:121 -- refused, no eviction
+        if (inserted) *inserted = 0;
+        return PG_OK;
+    }
+    PG_CUDA_THROW(cudaMemcpyAsync(c->emb + c->size * c->d, emb, (size_t)c->d * 8,
+                                  on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                  as_stream(s)));
+    c->size += 1;
+    if (inserted) *inserted = 1;
+    PG_API_END
+}
+
+int pg_cache_load(pg_cache c, const double* emb, size_t N) {
+    PG_API_BEGIN
+    require(c && (emb || N == 0), PG_INVALID_ARGUMENT, "cache: bad arguments");
+    require(N <= c->capacity, PG_INVALID_ARGUMENT, "cache: more entries than capacity");
+    if (N) PG_CUDA_THROW(cudaMemcpy(c->emb, emb, N * c->d * 8, cudaMemcpyHostToDevice));
+    c->size = N;
+    PG_API_END
+}
+
+int pg_retrieve(pg_cache c, const double* q, int exact_sim, pg_retrieve_result* res,
+                int32_t* entry_dev, int32_t* hit_dev, pg_stream s) {
+    PG_API_BEGIN
+    require(c && q, PG_INVALID_ARGUMENT, "retrieve: bad arguments");
+    if (c->size == 0) throw Error{PG_RUNTIME_ERROR, "empty cache"};
+    const cudaStream_t st = as_stream(s);
+    launch_cosine_scan(c->emb, q, (int)c->size, c->d, c->sim, c->bnd, st);
+    launch_retrieve_select(c->sim, c->bnd, c->emb, q, (int)c->size, c->d, c->min_sim, exact_sim,
+                           c->out_f64, c->out_i32, entry_dev, hit_dev, st);
+    if (res) {
+        PG_CUDA_THROW(cudaMemcpyAsync(c->pinned_f64, c->out_f64, 8, cudaMemcpyDeviceToHost, st));
+        PG_CUDA_THROW(cudaMemcpyAsync(c->pinned_i32, c->out_i32, 16, cudaMemcpyDeviceToHost, st));
+        PG_CUDA_THROW(cudaStreamSynchronize(st));
+        res->similarity = c->pinned_f64[0];
+        res->entry = (size_t)c->pinned_i32[0];
+        res->hit = c->pinned_i32[1];
+        res->exact_similarity = c->pinned_i32[2];
+    }
+    PG_API_END
+}
+
+int pg_embed_normalize(const void* x, pg_dtype dt, pg_layout lay, size_t d, size_t T, double* emb,
+                       pg_stream s) {
+    PG_API_BEGIN
+    require(x && emb && d > 0, PG_INVALID_ARGUMENT, "embed_prompt: bad arguments");
+    require(T > 0, PG_INVALID_ARGUMENT, "embed_prompt: empty prompt");
+    const cudaStream_t st = as_stream(s);
+    Scratch ws(32, st);
+    int64_t offs[2] = {0, (int64_t)T};
+    PG_CUDA_THROW(cudaMemcpyAsync(ws.p, offs, 16, cudaMemcpyHostToDevice, st));
+    launch_mean_pool(x, dt, lay, (int)d, (int64_t)T, ws.as<int64_t>(), 1, emb, st);
+    int* flag = reinterpret_cast<int*>(ws.as<int64_t>() + 2);
+    launch_embed_finish(emb, (int)d, flag, st);
+    int hflag = 0;
+    PG_CUDA_THROW(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st));
+    PG_CUDA_THROW(cudaStreamSynchronize(st));
+    if (hflag) throw Error{PG_RUNTIME_ERROR, "degenerate embedding"};
+    PG_API_END
+}
+
+// ------------------------------------------------------------ layers
+static int64_t padded_ld(size_t cols, pg_dtype dt) {
+    const size_t per = 16 / dtype_size(dt);
+    return (int64_t)round_up(cols, per);
+}
+
+int pg_layer_create(pg_layer* out, size_t m, size_t n, size_t r, size_t K, const double* A,
+                    const double* B, pg_dtype dt) {
+    PG_API_BEGIN
+    require(out && A && B && m && n && r, PG_INVALID_ARGUMENT, "layer: bad arguments");
+    require(K <= r, PG_INVALID_ARGUMENT, "layer: K > r_store");
+    const size_t es = dtype_size(dt);
+    const int64_t ldb = padded_ld(n, dt), lda = padded_ld(r, dt);
+    // B (n x r) -> B^T (r x ldb); A (m x r) -> (m x lda)
+    std::vector<double> bt((size_t)r * ldb, 0.0), ap((size_t)m * lda, 0.0);
+    for (size_t j = 0; j < n; ++j)
+        for (size_t e = 0; e < r; ++e) bt[e * ldb + j] = B[j * r + e];
+    for (size_t i = 0; i < m; ++i)
+        for (size_t e = 0; e < r; ++e) ap[i * lda + e] = A[i * r + e];
+    std::vector<unsigned char> tb(bt.size() * es), ta(ap.size() * es);
+    convert_store(bt.data(), bt.size(), dt, tb.data());
+    convert_store(ap.data(), ap.size(), dt, ta.data());
+    auto* L = new pg_layer_s{(int)m, (int)n, (int)r, (int)K, dt, nullptr, ldb, nullptr, lda, true};
+    L->bt = dev_alloc(tb.size());
+    L->a = dev_alloc(ta.size());
+    PG_CUDA_THROW(cudaMemcpy(L->bt, tb.data(), tb.size(), cudaMemcpyHostToDevice));
+    PG_CUDA_THROW(cudaMemcpy(L->a, ta.data(), ta.size(), cudaMemcpyHostToDevice));
+    *out = L;
+    PG_API_END
+}
+
+int pg_layer_create_device(pg_layer* out, size_t m, size_t n, size_t r, size_t K, const void* bt,
+                           const void* a, pg_dtype dt, int copy) {
+    PG_API_BEGIN
+    require(out && bt && a && m && n && r, PG_INVALID_ARGUMENT, "layer: bad arguments");
+    require(K <= r, PG_INVALID_ARGUMENT, "layer: K > r_store");
+    const size_t es = dtype_size(dt);
+    auto* L = new pg_layer_s{(int)m, (int)n, (int)r, (int)K, dt, const_cast<void*>(bt), (int64_t)n,
+                             const_cast<void*>(a), (int64_t)r, false};
+    const int64_t ldb = padded_ld(n, dt), lda = padded_ld(r, dt);
+    if (copy || ldb != (int64_t)n || lda != (int64_t)r) {
+        L->bt = dev_alloc((size_t)r * ldb * es);
+        L->a = dev_alloc((size_t)m * lda * es);
+        PG_CUDA_THROW(cudaMemset(L->bt, 0, (size_t)r * ldb * es));
+        PG_CUDA_THROW(cudaMemset(L->a, 0, (size_t)m * lda * es));
+        PG_CUDA_THROW(cudaMemcpy2D(L->bt, ldb * es, bt, n * es, n * es, r, cudaMemcpyDeviceToDevice));
+        PG_CUDA_THROW(cudaMemcpy2D(L->a, lda * es, a, r * es, r * es, m, cudaMemcpyDeviceToDevice));
+        L->ldb = ldb;
+        L->lda = lda;
+        L->owned = true;
+    }
+    *out = L;
+    PG_API_END
+}
+
+int pg_layer_destroy(pg_layer L) {
+    PG_API_BEGIN
+    if (!L) return PG_OK;
+    if (L->owned) {
+        cudaFree(L->bt);
+        cudaFree(L->a);
+    }
+    delete L;
+    PG_API_END
+}
+
+int pg_layer_info(pg_layer L, size_t* m, size_t* n, size_t* r, size_t* K, pg_dtype* dt) {
+    PG_API_BEGIN
+    require(L, PG_INVALID_ARGUMENT, "layer: null");
+    if (m) *m = L->m;
+    if (n) *n = L->n;
+    if (r) *r = L->r;
+    if (K) *K = L->K;
+    if (dt) *dt = L->dt;
+    PG_API_END
+}
+
+static void check_sel_host(const uint32_t* sel, size_t k, size_t r) {  // rank_experts.hpp:30-37
+    if (k == 0) throw Error{PG_INVALID_ARGUMENT, "selection must be non-empty"};
+    for (size_t i = 1; i < k; ++i)
+        if (sel[i] <= sel[i - 1])
+            throw Error{PG_INVALID_ARGUMENT, "selection indices not strictly increasing"};
+    if (sel[k - 1] >= r) throw Error{PG_OUT_OF_RANGE, "selection index beyond r_store"};
+}
+
+int pg_check_selection(pg_layer L, const uint32_t* sel, size_t k) {
+    PG_API_BEGIN
+    require(L, PG_INVALID_ARGUMENT, "layer: null");
+    check_sel_host(sel, k, (size_t)L->r);
+    PG_API_END
+}
+
+static void check_ydt(pg_dtype wdt, pg_dtype ydt) {
+    if (!(ydt == wdt || ydt == PG_F32 || (wdt == PG_F64 && ydt == PG_F64)))
+        throw Error{PG_INVALID_ARGUMENT, "forward: unsupported output dtype"};
+    if (wdt == PG_F64 && ydt != PG_F64)
+        throw Error{PG_INVALID_ARGUMENT, "forward: f64 layers produce f64 output"};
+}
+
+// Two-stage contraction over a slot map: decode GEMV when T is small and the
+// operands fit shared memory, SIMT GEMM otherwise (bf16 large-T goes to the
+// tensor-core path once enabled).
+static void run_forward(pg_dtype wdt, const void* bt, int64_t ldb, const void* a, int64_t lda,
+                        SlotMap sm, int nslots_max, int n, int m, const void* x, int fm, int T,
+                        void* y, pg_dtype ydt, cudaStream_t st) {
+    if (T == 0) return;
+    const size_t accs = wdt == PG_F64 ? 8 : 4;
+    if (decode_tmax(T) && decode_smem_need(wdt, n, nslots_max, T) <= 200 * 1024) {
+        Scratch z((size_t)nslots_max * T * accs, st);
+        launch_decode(wdt, bt, ldb, a, lda, sm, n, m, x, fm, T, z.p, y, ydt, st);
+        return;
+    }
+    Scratch ws(simt_ws_elems(n, m, nslots_max, T) * accs, st);
+    launch_simt(wdt, bt, ldb, a, lda, sm, n, m, x, fm, T, ws.p, y, ydt, st);
+}
+
+int pg_masked_forward(pg_layer L, const uint32_t* sel, size_t k, int sel_on_dev, const void* x,
+                      pg_layout lay, size_t T, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(L && sel && x && y, PG_INVALID_ARGUMENT, "masked_forward: bad X shape");
+    if (!sel_on_dev) check_sel_host(sel, k, (size_t)L->r);
+    else require(k > 0 && k <= (size_t)L->r, PG_INVALID_ARGUMENT, "selection must be non-empty");
+    check_ydt(L->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const int fm = lay == PG_FEATURE_MAJOR && T > 1;
+    const int ki = (int)k;
+    Scratch idx(k * 4, st);
+    PG_CUDA_THROW(cudaMemcpyAsync(idx.p, sel, k * 4, sel_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (decode_tmax((int)T) && decode_smem_need(L->dt, L->n, ki, (int)T) <= 200 * 1024) {
+        SlotMap sm;
+        sm.idx = idx.as<int32_t>();
+        sm.run0_len = ki;
+        run_forward(L->dt, L->bt, L->ldb, L->a, L->lda, sm, ki, L->n, L->m, x, fm, (int)T, y, ydt, st);
+        return PG_OK;
+    }
+    // large T: expert gather into a packed [K_pad] arena, then the GEMM path
+    const int kp = (int)round_up(k, kSlotAlign);
+    const size_t es = dtype_size(L->dt);
+    Scratch pb((size_t)kp * L->ldb * es, st), pa((size_t)L->m * kp * es, st);
+    launch_gather_rows(L->dt, L->bt, L->ldb, idx.as<int32_t>(), ki, kp, L->n, pb.p, L->ldb, st);
+    launch_gather_cols(L->dt, L->a, L->lda, idx.as<int32_t>(), ki, kp, L->m, pa.p, kp, st);
+    SlotMap sm;
+    sm.run0_len = kp;
+    run_forward(L->dt, pb.p, L->ldb, pa.p, kp, sm, kp, L->n, L->m, x, fm, (int)T, y, ydt, st);
+    PG_API_END
+}
+
+// ------------------------------------------------------------ aggregated layout
+int pg_aggregate_layout(pg_agg* out, pg_layer L, const uint32_t* pats, const size_t* ks, size_t P,
+                        double psi, pg_stream s) {
+    PG_API_BEGIN
+    require(out && L, PG_INVALID_ARGUMENT, "aggregate_layout: bad arguments");
+    if (P == 0) throw Error{PG_INVALID_ARGUMENT, "aggregate_layout: no patterns"};
+    if (psi <= 0 || psi > 1) throw Error{PG_INVALID_ARGUMENT, "aggregate_layout: psi out of range"};
+    const size_t r = L->r;
+    std::vector<size_t> freq(r, 0);
+    size_t off = 0;
+    for (size_t p = 0; p < P; ++p) {
+        for (size_t q = 0; q < ks[p]; ++q) {
+            const uint32_t e = pats[off + q];
+            if (e >= r) throw Error{PG_OUT_OF_RANGE, "pattern references expert >= r_store"};
+            freq[e] += 1;
+        }
+        off += ks[p];
+    }
+    auto g = std::make_unique<pg_agg_s>();
+    g->layer = L;
+    g->m = L->m;
+    g->n = L->n;
+    g->P = (int)P;
+    g->dt = L->dt;
+    for (size_t e = 0; e < r; ++e)
+        if (double(freq[e]) >= psi * double(P)) g->shared_ids.push_back((uint32_t)e);
+    const size_t sc = g->shared_ids.size();
+    g->s_pad = (int)round_up(sc, kSlotAlign);
+    g->res_ids.resize(P);
+    g->use_shared.resize(P);
+    g->ref_offset.resize(P);
+    g->dev_off.resize(P);
+    g->cnt_pad.resize(P);
+    size_t arena_ref = sc;
+    int arena_dev = g->s_pad;
+    off = 0;
+    for (size_t p = 0; p < P; ++p) {
+        g->use_shared[p].assign(sc, 0);
+        for (size_t q = 0; q < ks[p]; ++q) {
+            const uint32_t e = pats[off + q];
+            auto it = std::lower_bound(g->shared_ids.begin(), g->shared_ids.end(), e);
+            if (it != g->shared_ids.end() && *it == e) g->use_shared[p][it - g->shared_ids.begin()] = 1;
+            else g->res_ids[p].push_back(e);
+        }
+        g->ref_offset[p] = arena_ref;
+        arena_ref += g->res_ids[p].size();
+        g->dev_off[p] = arena_dev;
+        g->cnt_pad[p] = (int)round_up(g->res_ids[p].size(), kSlotAlign);
+        arena_dev += g->cnt_pad[p];
+        off += ks[p];
+    }
+    g->arena_cols = arena_dev;
+    // gather list over the device arena (-1 = zero padding)
+    std::vector<int32_t> idx(arena_dev, -1);
+    for (size_t j = 0; j < sc; ++j) idx[j] = (int32_t)g->shared_ids[j];
+    for (size_t p = 0; p < P; ++p)
+        for (size_t j = 0; j < g->res_ids[p].size(); ++j) idx[g->dev_off[p] + j] = (int32_t)g->res_ids[p][j];
+    std::vector<uint8_t> masks((size_t)P * g->s_pad, 0);
+    std::vector<int32_t> table(2 * P);
+    for (size_t p = 0; p < P; ++p) {
+        for (size_t j = 0; j < sc; ++j) masks[p * g->s_pad + j] = g->use_shared[p][j];
+        table[2 * p] = g->dev_off[p];
+        table[2 * p + 1] = g->cnt_pad[p];
+    }
+    const size_t es = dtype_size(L->dt);
+    g->ldb = L->ldb;
+    g->lda = arena_dev;  // multiple of 32 elements -> 16-byte aligned rows
+    g->bt_arena = dev_alloc((size_t)arena_dev * g->ldb * es);
+    g->a_arena = dev_alloc((size_t)g->m * g->lda * es);
+    g->masks = static_cast<uint8_t*>(dev_alloc(masks.size()));
+    g->table = static_cast<int32_t*>(dev_alloc(table.size() * 4));
+    g->bytes = (size_t)arena_dev * (g->ldb + g->m) * es;
+    const cudaStream_t st = as_stream(s);
+    PG_CUDA_THROW(cudaMemcpy(g->masks, masks.data(), masks.size(), cudaMemcpyHostToDevice));
+    PG_CUDA_THROW(cudaMemcpy(g->table, table.data(), table.size() * 4, cudaMemcpyHostToDevice));
+    Scratch di(idx.size() * 4, st);
+    PG_CUDA_THROW(cudaMemcpyAsync(di.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, st));
+    launch_gather_rows(L->dt, L->bt, L->ldb, di.as<int32_t>(), arena_dev, arena_dev, L->n, g->bt_arena,
+                       g->ldb, st);
+    launch_gather_cols(L->dt, L->a, L->lda, di.as<int32_t>(), arena_dev, arena_dev, L->m, g->a_arena,
+                       g->lda, st);
+    PG_CUDA_THROW(cudaStreamSynchronize(st));  // idx is host-owned until the copy lands
+    *out = g.release();
+    PG_API_END
+}
+
+int pg_agg_destroy(pg_agg g) {
+    PG_API_BEGIN
+    if (!g) return PG_OK;
+    cudaFree(g->bt_arena); cudaFree(g->a_arena); cudaFree(g->masks); cudaFree(g->table);
+    delete g;
+    PG_API_END
+}
+
+int pg_agg_patterns(pg_agg g, size_t* n) {
+    PG_API_BEGIN
+    require(g && n, PG_INVALID_ARGUMENT, "agg: bad arguments");
+    *n = g->P;
+    PG_API_END
+}
+
+int pg_agg_shared(pg_agg g, size_t* count, uint32_t* ids) {
+    PG_API_BEGIN
+    require(g && count, PG_INVALID_ARGUMENT, "agg: bad arguments");
+    *count = g->shared_ids.size();
+    if (ids) std::copy(g->shared_ids.begin(), g->shared_ids.end(), ids);
+    PG_API_END
+}
+
+int pg_agg_residual(pg_agg g, size_t p, size_t* count, uint32_t* ids, size_t* arena_offset,
+                    uint8_t* use_shared) {
+    PG_API_BEGIN
+    require(g, PG_INVALID_ARGUMENT, "agg: bad arguments");
+    if (p >= (size_t)g->P) throw Error{PG_OUT_OF_RANGE, "unknown pattern"};
+    if (count) *count = g->res_ids[p].size();
+    if (ids) std::copy(g->res_ids[p].begin(), g->res_ids[p].end(), ids);
+    if (arena_offset) *arena_offset = g->ref_offset[p];
+    if (use_shared) std::copy(g->use_shared[p].begin(), g->use_shared[p].end(), use_shared);
+    PG_API_END
+}
+
+int pg_agg_trace(pg_agg g, size_t p, size_t* count, size_t* cols) {
+    PG_API_BEGIN
+    require(g && count, PG_INVALID_ARGUMENT, "agg: bad arguments");
+    if (p >= (size_t)g->P) throw Error{PG_OUT_OF_RANGE, "unknown pattern"};
+    // one coalesced shared-block read [0, s) plus the pattern's residual block
+    // (exec_engine.hpp:201-213), reported in the reference's arena numbering
+    const size_t sc = g->shared_ids.size(), rc = g->res_ids[p].size();
+    *count = sc + rc;
+    if (cols) {
+        for (size_t j = 0; j < sc; ++j) cols[j] = j;
+        for (size_t j = 0; j < rc; ++j) cols[sc + j] = g->ref_offset[p] + j;
+    }
+    PG_API_END
+}
+
+int pg_agg_bytes(pg_agg g, size_t* bytes) {
+    PG_API_BEGIN
+    require(g && bytes, PG_INVALID_ARGUMENT, "agg: bad arguments");
+    *bytes = g->bytes;
+    PG_API_END
+}
+
+static SlotMap agg_slotmap(pg_agg g, int p) {
+    SlotMap sm;
+    sm.run0_len = g->s_pad;
+    sm.run1_start = g->dev_off[p];
+    sm.run1_len = g->cnt_pad[p];
+    sm.mask = g->masks + (size_t)p * g->s_pad;
+    return sm;
+}
+
+int pg_aggregated_forward(pg_agg g, size_t p, const int32_t* pdev, const void* x, pg_layout lay,
+                          size_t T, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(g && x && y, PG_INVALID_ARGUMENT, "aggregated_forward: bad X shape");
+    check_ydt(g->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const int fm = lay == PG_FEATURE_MAJOR && T > 1;
+    int maxcnt = 0;
+    for (int c : g->cnt_pad) maxcnt = std::max(maxcnt, c);
+    if (pdev) {
+        if (decode_tmax((int)T) && decode_smem_need(g->dt, g->n, g->s_pad + maxcnt, (int)T) <= 200 * 1024) {
+            SlotMap sm;
+            sm.run0_len = g->s_pad;
+            sm.dyn_pattern = pdev;
+            sm.dyn_table = g->table;
+            sm.dyn_masks = g->masks;
+            sm.dyn_mask_stride = g->s_pad;
+            run_forward(g->dt, g->bt_arena, g->ldb, g->a_arena, g->lda, sm, g->s_pad + maxcnt, g->n,
+                        g->m, x, fm, (int)T, y, ydt, st);
+            return PG_OK;
+        }
+        int32_t hp = 0;
+        PG_CUDA_THROW(cudaMemcpyAsync(&hp, pdev, 4, cudaMemcpyDeviceToHost, st));
+        PG_CUDA_THROW(cudaStreamSynchronize(st));
+        p = (size_t)hp;
+    }
+    if (p >= (size_t)g->P) throw Error{PG_OUT_OF_RANGE, "unknown pattern"};
+    SlotMap sm = agg_slotmap(g, (int)p);
+    run_forward(g->dt, g->bt_arena, g->ldb, g->a_arena, g->lda, sm, sm.nslots(), g->n, g->m, x, fm,
+                (int)T, y, ydt, st);
+    PG_API_END
+}
+
+int pg_aggregated_forward_batched(pg_agg g, const int32_t* pats, const int64_t* offs, size_t P,
+                                  const void* x, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(g && pats && offs && x && y, PG_INVALID_ARGUMENT, "aggregated_forward: bad X shape");
+    check_ydt(g->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const size_t es = dtype_size(g->dt), ys = dtype_size(ydt);
+    for (size_t q = 0; q < P; ++q) {
+        const int p = pats[q];
+        if (p < 0 || p >= g->P) throw Error{PG_OUT_OF_RANGE, "unknown pattern"};
+        const int64_t t0 = offs[q], t1 = offs[q + 1];
+        if (t1 <= t0) continue;
+        SlotMap sm = agg_slotmap(g, p);
+        run_forward(g->dt, g->bt_arena, g->ldb, g->a_arena, g->lda, sm, sm.nslots(), g->n, g->m,
+                    static_cast<const char*>(x) + t0 * g->n * es, 0, (int)(t1 - t0),
+                    static_cast<char*>(y) + t0 * g->m * ys, ydt, st);
+    }
+    PG_API_END
+}
+
+int pg_silu_mul(const void* g, const void* u, pg_dtype in_dt, size_t count, void* act,
+                pg_dtype act_dt, pg_stream s) {
+    PG_API_BEGIN
+    require(g && u && act, PG_INVALID_ARGUMENT, "silu_mul: null");
+    require(in_dt == PG_F32 || in_dt == PG_F64, PG_INVALID_ARGUMENT, "silu_mul: inputs must be f32/f64");
+    if (count) launch_silu_mul(g, u, in_dt, count, act, act_dt, as_stream(s));
+    PG_API_END
+}
+
+int pg_fill_normal_device(void* out, pg_dtype dt, size_t count, uint64_t seed, double scale,
+                          pg_stream s) {
+    PG_API_BEGIN
+    require(out, PG_INVALID_ARGUMENT, "fill: null");
+    launch_fill_normal(out, dt, count, seed, scale, as_stream(s));
+    PG_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+// route.cu -- K1: mean_pool -> score -> select_topk on sm_100a, bit-identical to
+// the reference's router (include/parse/router.hpp:41-61,80-88).
+//
+// Roofline: the router GEMV streams theta (r x n f64, 8*r*n bytes per prompt
+// batch) once -- HBM-bound.  mean_pool and the top-K are small.
+//
+// Exactness strategy (SURVEY.md §7 "Hard parts" 1):
+//  * mean_pool is computed in the reference's order (one thread per feature,
+//    sequential over tokens, __dadd_rn, one final __ddiv_rn) -- cheap.
+//  * score runs as a fast warp-tree FMA GEMV that also accumulates
+//    S_i = sum_j |theta_ij h_j|.  Both the reference's sequential dot and ours
+//    are within gamma_{n+1} (S_i + |b_i|) of the exact value, so
+//    |z_fast - z_ref| <= e_i := 4 (n+2) u (S_i + |b_i|) (+ denormal slack).
+//  * select: L = K-th largest fast logit, e = max_i e_i.  Rows with
+//    |z_i - L| > 2e are on the same side of the exact K-th value as in the
+//    reference; rows inside the band are recomputed in reference order
+//    (sequential __dmul_rn/__dadd_rn) unless the band is wholly selected.  The
+//    final top-K over the mixed vector equals the reference's top-K, including
+//    the lower-index tie rule (router.hpp:53-55) and ascending output (:57).
+#include "block_utils.cuh"
+
+namespace pg {
+
+// ---------------- mean_pool (router.hpp:80-88) ----------------
+
+template <typename TX>
+__global__ void k_mean_pool_tm(const TX* __restrict__ x, int n, const int64_t* __restrict__ offs,
+                               double* __restrict__ h) {
+    const int p = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t t0 = offs[p], t1 = offs[p + 1];
+    double s = 0.0;
+    for (int64_t t = t0; t < t1; ++t) s = __dadd_rn(s, to_d(x[t * (int64_t)n + i]));
+    h[(int64_t)p * n + i] = __ddiv_rn(s, (double)(t1 - t0));
+}
+
+// feature-major x [n, Ttot]: each warp owns 32 rows; a 32x32 tile is read
+// coalesced along tokens, then each lane sums its own row in token order.
+template <typename TX>
+__global__ void k_mean_pool_fm(const TX* __restrict__ x, int n, int64_t ttot,
+                               const int64_t* __restrict__ offs, double* __restrict__ h) {
+    __shared__ double tile[4][32][33];
+    const int p = blockIdx.y;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row0 = (blockIdx.x * 4 + w) * 32;
+    if (row0 >= n) return;
+    const int64_t t0 = offs[p], t1 = offs[p + 1];
+    double s = 0.0;
+    for (int64_t tc = t0; tc < t1; tc += 32) {
+        const int cnt = (int)((t1 - tc) < 32 ? (t1 - tc) : 32);
+        for (int rr = 0; rr < 32; ++rr) {
+            const int row = row0 + rr;
+            double v = 0.0;
+            if (row < n && lane < cnt) v = to_d(x[(int64_t)row * ttot + tc + lane]);
+            tile[w][rr][lane] = v;
+        }
+        __syncwarp();
+        for (int c = 0; c < cnt; ++c) s = __dadd_rn(s, tile[w][lane][c]);
+        __syncwarp();
+    }
+    const int row = row0 + lane;
+    if (row < n) h[(int64_t)p * n + row] = __ddiv_rn(s, (double)(t1 - t0));
+}
+
+// ---------------- score (router.hpp:41-46) ----------------
+
+constexpr int kScoreWarps = 8;
+constexpr int kScoreChunkP = 4;  // prompts per pass
+
+// fast: one warp per theta row, 16-byte loads, FMA tree; also the bound.
+__global__ void __launch_bounds__(kScoreWarps * 32)
+k_score_fast(const double* __restrict__ theta, const double* __restrict__ bias, int r, int n,
+             const double* __restrict__ h, int P, double* __restrict__ z,
+             double* __restrict__ bnd) {
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * kScoreWarps + (threadIdx.x >> 5);
+    if (row >= r) return;
+    const double* th = theta + (int64_t)row * n;
+    const double gam = 4.0 * (double)(n + 2) * kU;
+    const double tiny = 4.0 * (double)(n + 2) * 4.9406564584124654e-324;
+    for (int p0 = 0; p0 < P; p0 += kScoreChunkP) {
+        const int np = min(kScoreChunkP, P - p0);
+        double acc[kScoreChunkP], sab[kScoreChunkP];
+#pragma unroll
+        for (int q = 0; q < kScoreChunkP; ++q) acc[q] = sab[q] = 0.0;
+        const bool vec = ((n & 1) == 0);
+        if (vec) {
+            for (int j = 2 * lane; j < n; j += 64) {
+                const double2 t = __ldg(reinterpret_cast<const double2*>(th + j));
+#pragma unroll
+                for (int q = 0; q < kScoreChunkP; ++q) {
+                    if (q < np) {
+                        const double2 hv =
+                            __ldg(reinterpret_cast<const double2*>(h + (int64_t)(p0 + q) * n + j));
+                        acc[q] = fma(t.x, hv.x, acc[q]);
+                        acc[q] = fma(t.y, hv.y, acc[q]);
+                        sab[q] += fabs(t.x * hv.x) + fabs(t.y * hv.y);
+                    }
+                }
+            }
+        } else {
+            for (int j = lane; j < n; j += 32) {
+                const double t = __ldg(th + j);
+#pragma unroll
+                for (int q = 0; q < kScoreChunkP; ++q) {
+                    if (q < np) {
+                        const double hv = __ldg(h + (int64_t)(p0 + q) * n + j);
+                        acc[q] = fma(t, hv, acc[q]);
+                        sab[q] += fabs(t * hv);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kScoreChunkP; ++q) {
+            acc[q] = warp_sum(acc[q]);
+            sab[q] = warp_sum(sab[q]);
+        }
+        if (lane == 0) {
+            const double b = bias[row];
+            for (int q = 0; q < np; ++q) {
+                z[(int64_t)(p0 + q) * r + row] = acc[q] + b;
+                if (bnd) bnd[(int64_t)(p0 + q) * r + row] = gam * (sab[q] + fabs(b)) * 1.0000001 + tiny;
+            }
+        }
+    }
+}
+
+// reference order: dot (matrix.hpp:189-193) then + bias; one lane per row,
+// theta tiles staged through shared memory so global reads stay coalesced.
+__device__ __forceinline__ double ref_dot_row(const double* __restrict__ th,
+                                              const double* __restrict__ hv, int n) {
+    double s = 0.0;
+    int j = 0;
+    for (; j + 8 <= n; j += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { a[q] = th[j + q]; b[q] = hv[j + q]; }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, __dmul_rn(a[q], b[q]));
+    }
+    for (; j < n; ++j) s = __dadd_rn(s, __dmul_rn(th[j], hv[j]));
+    return s;
+}
+
+__global__ void k_score_exact(const double* __restrict__ theta, const double* __restrict__ bias,
+                              int r, int n, const double* __restrict__ h, int P,
+                              double* __restrict__ z) {
+    __shared__ double tile[4][32][33];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row0 = (blockIdx.x * 4 + w) * 32;
+    const int p = blockIdx.y;
+    if (row0 >= r) return;
+    const double* hv = h + (int64_t)p * n;
+    double s = 0.0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int cnt = min(32, n - j0);
+        for (int rr = 0; rr < 32; ++rr) {
+            const int row = row0 + rr;
+            tile[w][rr][lane] = (row < r && lane < cnt) ? theta[(int64_t)row * n + j0 + lane] : 0.0;
+        }
+        __syncwarp();
+        for (int c = 0; c < cnt; ++c) s = __dadd_rn(s, __dmul_rn(tile[w][lane][c], hv[j0 + c]));
+        __syncwarp();
+    }
+    const int row = row0 + lane;
+    if (row < r) z[(int64_t)p * r + row] = __dadd_rn(s, bias[row]);
+}
+
+// ---------------- select_topk (router.hpp:49-61) ----------------
+
+constexpr int kSelThreads = 1024;
+
+// Final exact top-K on zs (smem) with (value desc, index asc) order; writes
+// ascending indices.  flags: r bytes smem.
+__device__ void topk_emit(const double* zs, int r, int K, uint64_t tkey, int need_eq,
+                          uint8_t* flags, int* scratch, uint32_t* out) {
+    // per-thread contiguous chunk keeps index order for the tie scan
+    const int per = (r + kSelThreads - 1) / kSelThreads;
+    const int b0 = threadIdx.x * per, b1 = min(r, b0 + per);
+    int eq = 0;
+    for (int i = b0; i < b1; ++i) eq += (f64_key(zs[i]) == tkey);
+    int tot;
+    int eq_before = block_excl_scan<kSelThreads>(eq, scratch, &tot);
+    int sel_cnt = 0;
+    for (int i = b0; i < b1; ++i) {
+        const uint64_t k = f64_key(zs[i]);
+        bool s = k > tkey;
+        if (k == tkey) {
+            s = eq_before < need_eq;
+            ++eq_before;
+        }
+        flags[i] = s;
+        sel_cnt += s;
+    }
+    int pos = block_excl_scan<kSelThreads>(sel_cnt, scratch, &tot);
+    for (int i = b0; i < b1; ++i)
+        if (flags[i]) out[pos++] = (uint32_t)i;
+}
+
+// Plain top-K on given logits (pg_select_topk): pure comparisons, exact.
+__global__ void __launch_bounds__(kSelThreads)
+k_select_topk(const double* __restrict__ logits, int r, int K, uint32_t* __restrict__ sel) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* zs = reinterpret_cast<double*>(smem);
+    uint8_t* flags = reinterpret_cast<uint8_t*>(zs + r);
+    __shared__ int hist[256];
+    __shared__ int selv[2];
+    __shared__ int scratch[40];
+    const int p = blockIdx.x;
+    for (int i = threadIdx.x; i < r; i += kSelThreads) zs[i] = logits[(int64_t)p * r + i];
+    __syncthreads();
+    int need_eq;
+    uint64_t tkey = radix_select_kth<kSelThreads>(zs, r, K, hist, selv, &need_eq);
+    topk_emit(zs, r, K, tkey, need_eq, flags, scratch, sel + (int64_t)p * K);
+}
+
+// Routing select with the error-bounded band (see file header).
+__global__ void __launch_bounds__(kSelThreads)
+k_route_select(const double* __restrict__ zfast, const double* __restrict__ bnd,
+               const double* __restrict__ theta, const double* __restrict__ bias,
+               const double* __restrict__ h, int r, int n, int K, uint32_t* __restrict__ sel,
+               double* __restrict__ logits_out, int* __restrict__ stats) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* zs = reinterpret_cast<double*>(smem);
+    int* band = reinterpret_cast<int*>(zs + r);
+    uint8_t* flags = reinterpret_cast<uint8_t*>(band + r);
+    __shared__ int hist[256];
+    __shared__ int selv[2];
+    __shared__ int scratch[40];
+    __shared__ double dscratch[33];
+    const int p = blockIdx.x;
+    const double* zf = zfast + (int64_t)p * r;
+    const double* bd = bnd + (int64_t)p * r;
+    double emax = 0.0;
+    for (int i = threadIdx.x; i < r; i += kSelThreads) {
+        zs[i] = zf[i];
+        emax = fmax(emax, bd[i]);
+    }
+    emax = block_max_f64<kSelThreads>(emax, dscratch);  // includes __syncthreads
+    int need_eq;
+    uint64_t tkey = radix_select_kth<kSelThreads>(zs, r, K, hist, selv, &need_eq);
+    int recomputed = 0;
+    if (emax > 0.0) {
+        const double L = key_f64(tkey);
+        const double e2 = 2.0 * emax * (1.0 + 1e-9);
+        const double hi = L + e2, lo = L - e2;
+        int g = 0, b = 0;
+        for (int i = threadIdx.x; i < r; i += kSelThreads) {
+            const double v = zs[i];
+            g += v > hi;
+            b += (v >= lo && v <= hi);
+        }
+        const int G = block_sum_int<kSelThreads>(g, scratch);
+        const int B = block_sum_int<kSelThreads>(b, scratch);
+        if (K - G != B) {
+            // compact band rows that carry rounding uncertainty, recompute them
+            int mine = 0;
+            const int per = (r + kSelThreads - 1) / kSelThreads;
+            const int b0 = threadIdx.x * per, b1 = min(r, b0 + per);
+            for (int i = b0; i < b1; ++i) mine += (zs[i] >= lo && zs[i] <= hi && bd[i] > 0.0);
+            int tot;
+            int pos = block_excl_scan<kSelThreads>(mine, scratch, &tot);
+            for (int i = b0; i < b1; ++i)
+                if (zs[i] >= lo && zs[i] <= hi && bd[i] > 0.0) band[pos++] = i;
+            __syncthreads();
+            const double* hv = h + (int64_t)p * n;
+            for (int q = threadIdx.x; q < tot; q += kSelThreads) {
+                const int i = band[q];
+                zs[i] = __dadd_rn(ref_dot_row(theta + (int64_t)i * n, hv, n), bias[i]);
+            }
+            recomputed = tot;
+            __syncthreads();
+            tkey = radix_select_kth<kSelThreads>(zs, r, K, hist, selv, &need_eq);
+        }
+    }
+    topk_emit(zs, r, K, tkey, need_eq, flags, scratch, sel + (int64_t)p * K);
+    if (logits_out)
+        for (int i = threadIdx.x; i < r; i += kSelThreads) logits_out[(int64_t)p * r + i] = zs[i];
+    if (stats && threadIdx.x == 0) stats[p] = recomputed;
+}
+
+// ---------------- host launchers ----------------
+
+template <typename TX>
+static void launch_mean_pool_t(const void* x, pg_layout lay, int n, int64_t ttot,
+                               const int64_t* offs_dev, int P, double* h, cudaStream_t st) {
+    if (lay == PG_TOKEN_MAJOR) {
+        dim3 g((n + 255) / 256, P);
+        k_mean_pool_tm<TX><<<g, 256, 0, st>>>(static_cast<const TX*>(x), n, offs_dev, h);
+    } else {
+        dim3 g((n + 127) / 128, P);
+        k_mean_pool_fm<TX><<<g, 128, 0, st>>>(static_cast<const TX*>(x), n, ttot, offs_dev, h);
+    }
+    PG_LAUNCH_CHECK();
+}
+
+void launch_mean_pool(const void* x, pg_dtype dt, pg_layout lay, int n, int64_t ttot,
+                      const int64_t* offs_dev, int P, double* h, cudaStream_t st) {
+    switch (dt) {
+        case PG_F64: launch_mean_pool_t<double>(x, lay, n, ttot, offs_dev, P, h, st); break;
+        case PG_F32: launch_mean_pool_t<float>(x, lay, n, ttot, offs_dev, P, h, st); break;
+        default: launch_mean_pool_t<__nv_bfloat16>(x, lay, n, ttot, offs_dev, P, h, st); break;
+    }
+}
+
+void launch_score(const double* theta, const double* bias, int r, int n, const double* h, int P,
+                  double* z, double* bnd, int exact, cudaStream_t st) {
+    if (exact) {
+        dim3 g((r + 127) / 128, P);
+        k_score_exact<<<g, 128, 0, st>>>(theta, bias, r, n, h, P, z);
+    } else {
+        k_score_fast<<<(r + kScoreWarps - 1) / kScoreWarps, kScoreWarps * 32, 0, st>>>(
+            theta, bias, r, n, h, P, z, bnd);
+    }
+    PG_LAUNCH_CHECK();
+}
+
+static size_t sel_smem(int r, bool band) {
+    return (size_t)r * 8 + (band ? (size_t)r * 4 : 0) + (size_t)r + 16;
+}
+
+void select_smem_setup() {
+    static bool done = false;
+    if (done) return;
+    PG_CUDA_THROW(cudaFuncSetAttribute(k_select_topk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+    PG_CUDA_THROW(cudaFuncSetAttribute(k_route_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+    done = true;
+}
+
+int max_select_rows() { return (200 * 1024 - 64) / 13; }
+
+void launch_select_topk(const double* logits, int r, int P, int K, uint32_t* sel, cudaStream_t st) {
+    select_smem_setup();
+    k_select_topk<<<P, kSelThreads, sel_smem(r, false), st>>>(logits, r, K, sel);
+    PG_LAUNCH_CHECK();
+}
+
+void launch_route_select(const double* zfast, const double* bnd, const double* theta,
+                         const double* bias, const double* h, int r, int n, int K, int P,
+                         uint32_t* sel, double* logits_out, int* stats, cudaStream_t st) {
+    select_smem_setup();
+    k_route_select<<<P, kSelThreads, sel_smem(r, true), st>>>(zfast, bnd, theta, bias, h, r, n, K,
+                                                              sel, logits_out, stats);
+    PG_LAUNCH_CHECK();
+}
+
+}  // namespace pg
