@@ -183,7 +183,7 @@ def gpu_arm(args, rank, world, local_rank):
     cache = pg.PatternCache(D_MODEL, N_CACHE, MIN_SIM)
     cache.load([pg.CacheEntry(pg.PromptEmbedding(e), {"up": p[0], "gate": p[1], "down": p[2]})
                 for e, p in zip(emb.cpu().numpy(), pats)])
-    q = emb[7] + 0.05 * torch.randn(D_MODEL, generator=gen, device=dev, dtype=torch.float64)
+    q = emb[7] + 0.3 / D_MODEL ** 0.5 * torch.randn(D_MODEL, generator=gen, device=dev, dtype=torch.float64)
     q /= q.norm()
 
     blocks = [build_block(pg, torch, sh, dev, 100 * rank + j) for j in range(REPLICAS)]
@@ -215,34 +215,38 @@ def gpu_arm(args, rank, world, local_rank):
     x_host.copy_(xs.cpu())
     y_host = torch.empty((G, D_MODEL), dtype=torch.float32).pin_memory()
 
-    def step(i, host_io):
+    def step(i, host_io, fused=True):
         a = aggs[i % REPLICAS]
         if host_io:
             xs[i].copy_(x_host[i], non_blocking=True)
-        pg.aggregated_forward(a["up"], 0, xs[i], out=up[i])
-        pg.aggregated_forward(a["gate"], 0, xs[i], out=gt[i])
-        pg.silu_mul(gt[i], up[i], out=act[i])
-        pg.aggregated_forward(a["down"], 0, act[i], out=y[i])
+        if fused:  # K6: whole MLP block in one kernel (up/gate fused B side, silu epilogue, down)
+            pg.mlp_forward(a["up"], a["gate"], a["down"], 0, xs[i], out=y[i], act=act[i])
+        else:      # aggregated-only: one chain kernel per linear + silu kernel
+            pg.aggregated_forward(a["up"], 0, xs[i], out=up[i])
+            pg.aggregated_forward(a["gate"], 0, xs[i], out=gt[i])
+            pg.silu_mul(gt[i], up[i], out=act[i])
+            pg.aggregated_forward(a["down"], 0, act[i], out=y[i])
         if host_io:
             y_host[i].copy_(y[i], non_blocking=True)
 
     stream = torch.cuda.Stream(device=dev)
     graphs = {}
-    for host_io in (False, True):
+    for key in ((False, True), (True, True), (False, False)):
+        host_io, fused = key
         with torch.cuda.stream(stream):
             for i in range(G):  # warm (kernel attributes, pools) outside capture
-                step(i, host_io)
+                step(i, host_io, fused)
         stream.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = pg.launch_count()
         with torch.cuda.graph(g, stream=stream):
             for i in range(G):
-                step(i, host_io)
-        graphs[host_io] = (g, pg.launch_count() - n0)
+                step(i, host_io, fused)
+        graphs[key] = (g, pg.launch_count() - n0)
     torch.cuda.synchronize()
 
-    def timed(host_io, steps):
-        g, _ = graphs[host_io]
+    def timed(host_io, steps, fused=True):
+        g, _ = graphs[(host_io, fused)]
         reps = max(1, steps // G)
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
@@ -270,25 +274,17 @@ def gpu_arm(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ms, nsteps = timed(False, args.steps)
     ms_e2e, nsteps_e2e = timed(True, args.steps)
-    launches_per_step = graphs[False][1] / G
+    ms_unf, nsteps_unf = timed(False, args.steps, fused=False)
+    launches_per_step = graphs[(False, True)][1] / G
 
-    # ---- roofline: the up-projection forward, CUDA events on its stream
-    m, n, K, r = sh["up"]
-    alg_bytes = K * (m + n) * 2 + n * 2 + m * 4
-    reps = 200
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        for i in range(8):
-            pg.aggregated_forward(aggs[i % REPLICAS]["up"], 0, xs[i], out=up[i])
-        e0.record(stream)
-        for i in range(reps):
-            pg.aggregated_forward(aggs[i % REPLICAS]["up"], 0, xs[i % G], out=up[i % G])
-        e1.record(stream)
-    torch.cuda.synchronize()
-    lin_us = e0.elapsed_time(e1) / reps * 1e3
-    achieved = alg_bytes / (lin_us * 1e-6) / 1e9
-
-    step_bytes = sum(K_ * (m_ + n_) * 2 for (m_, n_, K_, _) in sh.values())
+    # ---- roofline: the dominant (only) kernel of the step is k_chain<bf16>, the
+    # fused MLP block; one launch per step, timed by CUDA events on its stream
+    # over the timed region.  Algorithmic bytes = sum_l K_l (m_l + n_l) * 2 (the
+    # selected experts' U and V rows) + x, act (write+read) and y.
+    lin_bytes = {k: K_ * (m_ + n_) * 2 for k, (m_, n_, K_, _) in sh.items()}
+    step_bytes = sum(lin_bytes.values()) + D_MODEL * 2 + D_FF * 2 * 2 + D_MODEL * 4
+    step_us = ms / nsteps * 1e3
+    achieved = step_bytes / (step_us * 1e-6) / 1e9
     tok_s = nsteps / (ms * 1e-3) * world
     out = {
         "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": nsteps,
@@ -305,11 +301,13 @@ def gpu_arm(args, rank, world, local_rank):
                 "h2d_bytes_per_step": D_MODEL * 2, "d2h_bytes_per_step": D_MODEL * 4},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None,
-                     "kernel": "up-projection forward (k_stage1_gemv + k_stage2_gemv, 2 launches)",
-                     "alg_bytes_per_launch": alg_bytes, "avg_us": lin_us, "peak_kind": peak_kind},
-        "step_roofline": {"alg_bytes_per_step": step_bytes,
-                          "achieved_GBps": step_bytes / (ms / nsteps * 1e-3) / 1e9,
-                          "frac": step_bytes / (ms / nsteps * 1e-3) / 1e9 / hbm_peak},
+                     "kernel": "k_chain<bf16> (fused MLP block: up+gate stage 1, grid barrier, stage 2 + "
+                               "silu epilogue, down stage 1/2; 1 launch per step)",
+                     "alg_bytes_per_launch": step_bytes, "avg_us": step_us, "peak_kind": peak_kind},
+        "variants": {"aggregated_fused_tok_s": tok_s,
+                     "aggregated_only_tok_s": nsteps_unf / (ms_unf * 1e-3) * world,
+                     "launches_per_step": {"fused": launches_per_step,
+                                           "unfused": graphs[(False, False)][1] / G}},
         "gpu_launches": int(launches_per_step * nsteps),
         "clocks": clk.summary(),
         "prefill_setup": {"retrieve_us": retrieve_us, "retrieve_plus_pack_ms_host": setup_ms},
@@ -353,7 +351,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = gpu_arm(args, rank, world, local_rank)
     if rank == 0:
-        if world == 1:
+        if world == 1 and args.cpu_steps > 0:
             ref = reference_arm(args.cpu_steps, 1)
             out["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(out), flush=True)

@@ -196,6 +196,23 @@ int pg_aggregated_forward_batched(pg_agg g, const int32_t* patterns_host,
                                   const void* x_dev, void* y_dev, pg_dtype y_dtype,
                                   pg_stream stream);
 
+/* K6 module fusion for decode (T = 1): build_plan's fused_B + batched_A groups
+ * (exec_engine.hpp:46-68) executed as ONE kernel -- 1..3 linears sharing the
+ * input x (e.g. {q,k,v} or {up,gate}); ys[l] receives linear l's output.
+ * patterns_host[l] selects each linear's pattern, or pattern_dev (int32 on
+ * device, same pattern id for all linears) overrides them. */
+int pg_module_forward(const pg_agg* layers, size_t n_linears, const size_t* patterns_host,
+                      const int32_t* pattern_dev, const void* x_dev, void* const* ys_dev,
+                      pg_dtype y_dtype, pg_stream stream);
+
+/* Whole MLP block decode step (T = 1) in one kernel: up/gate share x (fused B
+ * side), act = silu(gate)*up in the stage-2 epilogue (toy_lm.hpp:250-257),
+ * then down_proj on act.  act_dev (nullable, m_ff elements of the storage
+ * dtype) receives the activation; y_dev the block output. */
+int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns_host,
+                   const int32_t* pattern_dev, const void* x_dev, void* act_dev, void* y_dev,
+                   pg_dtype y_dtype, pg_stream stream);
+
 /* MLP glue between upgate() and down_proj() (toy_lm.hpp:250-257):
  * act[i] = silu(gate[i]) * up[i], computed in f32 (f64 for f64 inputs) and
  * stored in act_dtype.  gate/up dtype in_dtype (PG_F32 or PG_F64). */

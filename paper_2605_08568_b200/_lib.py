@@ -75,6 +75,8 @@ _SIGS = {
     "pg_aggregated_forward_batched": [_vp, _i32p, _i64p, _sz, _vp, _vp, _i, _vp],
     "pg_fill_normal_device": [_vp, _i, _sz, C.c_uint64, C.c_double, _vp],
     "pg_silu_mul": [_vp, _vp, _i, _sz, _vp, _i, _vp],
+    "pg_module_forward": [C.POINTER(_vp), _sz, _sp, _vp, _vp, C.POINTER(_vp), _i, _vp],
+    "pg_mlp_forward": [_vp, _vp, _vp, _sp, _vp, _vp, _vp, _vp, _i, _vp],
 }
 _VOID = {
     "pg_rng_fill_gaussian": [C.c_uint64, _dp, _sz],

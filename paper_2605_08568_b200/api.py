@@ -725,6 +725,42 @@ class ExecProvider(ProjectionProvider):
         return self.eng.forward(tensor_id(b, p), self.pattern, x, self.variant, layout=self.layout)
 
 
+def _pattern_args(pattern_ids, count):
+    if isinstance(pattern_ids, torch.Tensor):
+        return None, _ptr(pattern_ids)
+    pats = [int(pattern_ids)] * count if np.isscalar(pattern_ids) else [int(p) for p in pattern_ids]
+    arr = (C.c_size_t * count)(*pats)
+    return arr, None
+
+
+def module_forward(aggs: list, pattern_ids, x: torch.Tensor, out_dtype=None, outs=None) -> list:
+    """K6 fused module (exec_engine.hpp:46-68 fused_B + batched_A), decode T=1:
+    1..3 linears sharing x run as one kernel.  pattern_ids: int, list, or a
+    device int32 tensor (retrieve_device's entry)."""
+    x = _dev(x, aggs[0].layer.torch_dtype).reshape(-1)
+    ydt = _out_dtype(aggs[0].layer.dtype, out_dtype)
+    ys = outs if outs is not None else [torch.empty(g.m, dtype=_TORCH[ydt], device=x.device) for g in aggs]
+    hs = (C.c_void_p * len(aggs))(*[g.handle.value for g in aggs])
+    yp = (C.c_void_p * len(aggs))(*[_ptr(y) for y in ys])
+    parr, pdev = _pattern_args(pattern_ids, len(aggs))
+    call("pg_module_forward", hs, len(aggs), parr, pdev, _ptr(x), yp, ydt, _stream())
+    return ys
+
+
+def mlp_forward(up: "AggregatedLayer", gate: "AggregatedLayer", down: "AggregatedLayer", pattern_ids,
+                x: torch.Tensor, out_dtype=None, out: torch.Tensor | None = None,
+                act: torch.Tensor | None = None) -> torch.Tensor:
+    """One decode token (T=1) through a rank-expert MLP block in ONE kernel:
+    up/gate share x, act = silu(gate)*up (toy_lm.hpp:250-257), y = down(act)."""
+    x = _dev(x, up.layer.torch_dtype).reshape(-1)
+    ydt = _out_dtype(up.layer.dtype, out_dtype)
+    y = out if out is not None else torch.empty(down.m, dtype=_TORCH[ydt], device=x.device)
+    parr, pdev = _pattern_args(pattern_ids, 3)
+    call("pg_mlp_forward", up.handle, gate.handle, down.handle, parr, pdev, _ptr(x),
+         _ptr(act) if act is not None else None, _ptr(y), ydt, _stream())
+    return y
+
+
 def silu_mul(gate: torch.Tensor, up: torch.Tensor, out_dtype=torch.bfloat16, out=None) -> torch.Tensor:
     """MLP glue (toy_lm.hpp:250-257): silu(gate) * up on device."""
     if gate.shape != up.shape or gate.dtype != up.dtype:

@@ -7,7 +7,7 @@
 #include <mutex>
 #include <vector>
 
-#include "pg_common.cuh"
+#include "chain.cuh"
 
 namespace pg {
 
@@ -265,11 +265,14 @@ int pg_route_select(pg_router R, const void* x, pg_dtype dt, pg_layout lay, cons
     require(R->r <= max_select_rows(), PG_INVALID_ARGUMENT, "select_topk: too many experts for device top-k");
     const cudaStream_t st = as_stream(s);
     const size_t r = R->r, n = R->n;
-    Scratch ws((P + 1) * 8 + P * n * 8 + 2 * P * r * 8, st);
+    // sub-buffers 256-byte aligned (the GEMV reads h / theta with 16-byte loads)
+    const size_t o_h = round_up((P + 1) * 8, 256), o_z = o_h + round_up(P * n * 8, 256),
+                 o_b = o_z + round_up(P * r * 8, 256);
+    Scratch ws(o_b + P * r * 8, st);
     int64_t* od = ws.as<int64_t>();
-    double* h = reinterpret_cast<double*>(od + P + 1);
-    double* z = h + P * n;
-    double* bnd = z + P * r;
+    double* h = reinterpret_cast<double*>(ws.as<char>() + o_h);
+    double* z = reinterpret_cast<double*>(ws.as<char>() + o_z);
+    double* bnd = reinterpret_cast<double*>(ws.as<char>() + o_b);
     PG_CUDA_THROW(cudaMemcpyAsync(od, offs, (P + 1) * 8, cudaMemcpyHostToDevice, st));
     launch_mean_pool(x, dt, lay, (int)n, offs[P], od, (int)P, h, st);
     launch_score(R->theta, R->bias, (int)r, (int)n, h, (int)P, z, bnd, 0, st);
@@ -491,13 +494,79 @@ static void check_ydt(pg_dtype wdt, pg_dtype ydt) {
 // Two-stage contraction over a slot map: decode GEMV when T is small and the
 // operands fit shared memory, SIMT GEMM otherwise (bf16 large-T goes to the
 // tensor-core path once enabled).
+// One linear of a decode chain (T = 1).
+struct LinSpec {
+    const void* bt;
+    int64_t ldb;
+    const void* a;
+    int64_t lda;
+    SlotMap sm;
+    int cap, n, m;
+    void* y;
+};
+
+// Single-launch decode chain (decode.cu).  phases[0] = linears sharing x; when
+// mlp is set, phase 0 is {up, gate} with the silu epilogue into act and phase
+// 1 is {down} reading act.
+static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, const void* x,
+                      bool mlp, void* act, pg_dtype ydt, cudaStream_t st) {
+    const size_t accs = wdt == PG_F64 ? 8 : 4, es = dtype_size(wdt);
+    ChainParams P = {};
+    P.nphase = (int)phases.size();
+    P.prefetch = 1;
+    size_t zbytes = 256, smem = 16;
+    std::vector<int> splits;
+    for (auto& ph : phases) {
+        int tot = 0;
+        for (auto& l : ph) tot += l.cap;
+        splits.push_back(chain_split(tot));
+        size_t zs = 0;
+        for (auto& l : ph) {
+            zbytes += round_up((size_t)l.cap * splits.back() * accs, 256);
+            zs += round_up(l.cap, 4) * accs;
+        }
+        smem = std::max({smem, (size_t)ph[0].n * es + 16, zs});
+    }
+    const size_t act_bytes = (mlp && !act) ? round_up((size_t)phases[0][0].m * es, 256) : 0;
+    Scratch ws(zbytes + act_bytes, st);
+    char* base = ws.as<char>();
+    PG_CUDA_THROW(cudaMemsetAsync(base, 0, 8, st));
+    P.bar = reinterpret_cast<unsigned long long*>(base);
+    size_t off = 256;
+    if (act_bytes) act = base + zbytes;
+    for (size_t p = 0; p < phases.size(); ++p) {
+        ChainPhase& Q = P.ph[p];
+        Q.nlin = (int)phases[p].size();
+        Q.split = splits[p];
+        Q.x = p == 0 ? x : act;
+        Q.epilogue = (mlp && p == 0) ? 1 : 0;
+        Q.ydt = ydt;
+        Q.act = act;
+        for (int l = 0; l < Q.nlin; ++l) {
+            const LinSpec& S = phases[p][l];
+            ChainLin& L = Q.lin[l];
+            L.bt = S.bt; L.ldb = S.ldb; L.a = S.a; L.lda = S.lda; L.sm = S.sm; L.cap = S.cap;
+            L.n = S.n; L.m = S.m; L.y = S.y;
+            L.zpart = base + off;
+            off += round_up((size_t)S.cap * Q.split * accs, 256);
+        }
+    }
+    if (smem > 200 * 1024) throw Error{PG_INVALID_ARGUMENT, "decode chain: operands exceed shared memory"};
+    launch_chain(wdt, P, smem, st);
+}
+
 static void run_forward(pg_dtype wdt, const void* bt, int64_t ldb, const void* a, int64_t lda,
                         SlotMap sm, int nslots_max, int n, int m, const void* x, int fm, int T,
                         void* y, pg_dtype ydt, cudaStream_t st) {
     if (T == 0) return;
     const size_t accs = wdt == PG_F64 ? 8 : 4;
+    if (T == 1 && (size_t)n * dtype_size(wdt) <= 190 * 1024 && (size_t)nslots_max * accs <= 190 * 1024) {
+        run_chain(wdt, {{LinSpec{bt, ldb, a, lda, sm, nslots_max, n, m, y}}}, x, false, nullptr, ydt, st);
+        return;
+    }
     if (decode_tmax(T) && decode_smem_need(wdt, n, nslots_max, T) <= 200 * 1024) {
         Scratch z((size_t)nslots_max * T * accs, st);
+        sm.cap = nslots_max;
         launch_decode(wdt, bt, ldb, a, lda, sm, n, m, x, fm, T, z.p, y, ydt, st);
         return;
     }
@@ -747,6 +816,59 @@ int pg_silu_mul(const void* g, const void* u, pg_dtype in_dt, size_t count, void
     require(g && u && act, PG_INVALID_ARGUMENT, "silu_mul: null");
     require(in_dt == PG_F32 || in_dt == PG_F64, PG_INVALID_ARGUMENT, "silu_mul: inputs must be f32/f64");
     if (count) launch_silu_mul(g, u, in_dt, count, act, act_dt, as_stream(s));
+    PG_API_END
+}
+
+static LinSpec agg_spec(pg_agg g, int p, const int32_t* pdev, void* y) {
+    SlotMap sm;
+    int cap;
+    if (pdev) {
+        sm.run0_len = g->s_pad;
+        sm.dyn_pattern = pdev;
+        sm.dyn_table = g->table;
+        sm.dyn_masks = g->masks;
+        sm.dyn_mask_stride = g->s_pad;
+        int maxcnt = 0;
+        for (int c : g->cnt_pad) maxcnt = std::max(maxcnt, c);
+        cap = g->s_pad + maxcnt;
+    } else {
+        if (p < 0 || p >= g->P) throw Error{PG_OUT_OF_RANGE, "unknown pattern"};
+        sm = agg_slotmap(g, p);
+        cap = sm.nslots();
+    }
+    return LinSpec{g->bt_arena, g->ldb, g->a_arena, g->lda, sm, cap, g->n, g->m, y};
+}
+
+int pg_module_forward(const pg_agg* gs, size_t nlin, const size_t* patterns, const int32_t* pattern_dev,
+                      const void* x, void* const* ys, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(gs && nlin >= 1 && nlin <= (size_t)kMaxLin && x && ys, PG_INVALID_ARGUMENT,
+            "module_forward: 1..3 linears sharing one input");
+    std::vector<LinSpec> ph;
+    for (size_t l = 0; l < nlin; ++l) {
+        require(gs[l] && gs[l]->dt == gs[0]->dt && gs[l]->n == gs[0]->n, PG_INVALID_ARGUMENT,
+                "module_forward: linears must share dtype and input width");
+        check_ydt(gs[l]->dt, ydt);
+        ph.push_back(agg_spec(gs[l], pattern_dev ? 0 : (int)patterns[l], pattern_dev, ys[l]));
+    }
+    run_chain(gs[0]->dt, {ph}, x, false, nullptr, ydt, as_stream(s));
+    PG_API_END
+}
+
+int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, const int32_t* pattern_dev,
+                   const void* x, void* act, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(up && gate && down && x && y, PG_INVALID_ARGUMENT, "mlp_forward: bad arguments");
+    require(up->dt == gate->dt && up->dt == down->dt, PG_INVALID_ARGUMENT, "mlp_forward: mixed dtypes");
+    require(up->m == gate->m && up->n == gate->n && down->n == up->m, PG_INVALID_ARGUMENT,
+            "mlp_forward: shape mismatch (up/gate m x n, down n x m)");
+    check_ydt(down->dt, ydt);
+    const int p0 = pattern_dev ? 0 : (int)patterns[0], p1 = pattern_dev ? 0 : (int)patterns[1],
+              p2 = pattern_dev ? 0 : (int)patterns[2];
+    run_chain(up->dt,
+              {{agg_spec(up, p0, pattern_dev, nullptr), agg_spec(gate, p1, pattern_dev, nullptr)},
+               {agg_spec(down, p2, pattern_dev, y)}},
+              x, true, act, ydt, as_stream(s));
     PG_API_END
 }
 

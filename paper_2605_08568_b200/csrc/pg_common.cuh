@@ -107,6 +107,7 @@ struct SlotMap {
     const int32_t* dyn_table = nullptr;
     const uint8_t* dyn_masks = nullptr;
     int dyn_mask_stride = 0;
+    int cap = 0;  // host-side upper bound on nslots (smem / grid sizing when dyn_pattern is set)
     __host__ __device__ int nslots() const { return idx ? run0_len : run0_len + run1_len; }
 };
 

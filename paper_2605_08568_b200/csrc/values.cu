@@ -475,7 +475,7 @@ template <typename W, int TM>
 static void decode_tm(const W* bt, int64_t ldb, const W* a, int64_t lda, SlotMap sm, int n, int m,
                       const W* x, int fm, int T, typename Acc<W>::type* z, void* y, pg_dtype ydt,
                       cudaStream_t st) {
-    const int ns = sm.nslots();
+    const int ns = sm.cap ? sm.cap : sm.nslots();
     stage1_t<W, TM>(bt, ldb, sm, ns, n, x, fm, T, z, st);
     if (ydt == PG_F32) stage2_t<W, float, TM>(a, lda, sm, ns, m, z, T, fm, static_cast<float*>(y), st);
     else if (ydt == PG_F64) stage2_t<W, double, TM>(a, lda, sm, ns, m, z, T, fm, static_cast<double*>(y), st);
