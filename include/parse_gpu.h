@@ -235,6 +235,10 @@ void pg_make_patterns(uint64_t seed, size_t n_patterns, const size_t* r_stores,
 int pg_fill_normal_device(void* out_dev, pg_dtype dtype, size_t count, uint64_t seed,
                           double scale, pg_stream stream);
 
+/* Diagnostics: with PG_CHAIN_DBG=1 the decode-chain kernel records per-CTA
+ * %globaltimer stamps [cta][16] of its phases; copies the last launch's. */
+int pg_chain_debug_dump(uint64_t* out_host, size_t n);
+
 #ifdef __cplusplus
 }
 #endif

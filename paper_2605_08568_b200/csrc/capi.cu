@@ -3,6 +3,7 @@
 // dispatch to the sm_100a kernels.
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -494,6 +495,20 @@ static void check_ydt(pg_dtype wdt, pg_dtype ydt) {
 // Two-stage contraction over a slot map: decode GEMV when T is small and the
 // operands fit shared memory, SIMT GEMM otherwise (bf16 large-T goes to the
 // tensor-core path once enabled).
+// Optional per-CTA phase timestamps (PG_CHAIN_DBG=1), read by pg_chain_debug_dump.
+static unsigned long long* g_chain_dbg = nullptr;
+static unsigned long long* chain_debug_buffer() {
+    static const bool on = [] {
+        const char* e = getenv("PG_CHAIN_DBG");
+        return e && atoi(e);
+    }();
+    if (on && !g_chain_dbg) {
+        PG_CUDA_THROW(cudaMalloc(&g_chain_dbg, 1024 * 16 * 8));
+        PG_CUDA_THROW(cudaMemset(g_chain_dbg, 0, 1024 * 16 * 8));
+    }
+    return on ? g_chain_dbg : nullptr;
+}
+
 // One linear of a decode chain (T = 1).
 struct LinSpec {
     const void* bt;
@@ -508,36 +523,99 @@ struct LinSpec {
 // Single-launch decode chain (decode.cu).  phases[0] = linears sharing x; when
 // mlp is set, phase 0 is {up, gate} with the silu epilogue into act and phase
 // 1 is {down} reading act.
+// Decode-chain workspace per (device, stream): [barrier counter | z | act].
+// Grows outside graph capture only; reused by every launch on that stream.
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, cudaStream_t>, std::pair<char*, size_t>> g_ws;
+static char* chain_workspace(cudaStream_t st, size_t bytes) {
+    int dev = 0;
+    PG_CUDA_THROW(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto& w = g_ws[{dev, st}];
+    if (w.second < bytes) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        PG_CUDA_THROW(cudaStreamIsCapturing(st, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            throw Error{PG_RUNTIME_ERROR, "decode chain: workspace must be sized by a call before graph capture"};
+        PG_CUDA_THROW(cudaStreamSynchronize(st));
+        if (w.first) PG_CUDA_THROW(cudaFree(w.first));
+        const size_t sz = round_up(bytes, 1 << 20);
+        PG_CUDA_THROW(cudaMalloc(&w.first, sz));
+        PG_CUDA_THROW(cudaMemset(w.first, 0, sz));
+        w.second = sz;
+    }
+    return w.first;
+}
+
+// Chain feasibility: contiguous runs only (no gather list) and the largest
+// streamed item (a B^T row, or an up/gate A-row pair) fits one ring stage.
+static size_t chain_chunk_bytes(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, bool mlp,
+                                size_t* xs_bytes, size_t* zs_bytes) {
+    const size_t accs = wdt == PG_F64 ? 8 : 4, es = dtype_size(wdt);
+    size_t xs = 16, zs = 16, item = 16;
+    for (size_t p = 0; p < phases.size(); ++p) {
+        const auto& ph = phases[p];
+        size_t zsum = 0, pair = 0;
+        for (const auto& l : ph) {
+            if (l.sm.idx) return 0;
+            xs = std::max(xs, round_up((size_t)l.n * es + 16, 128));
+            zsum += round_up(l.cap, 4) * accs;
+            item = std::max(item, (size_t)l.ldb * es);
+            item = std::max(item, (size_t)l.cap * es);
+            pair += (size_t)l.cap * es;
+        }
+        if (mlp && p == 0) item = std::max(item, pair);
+        zs = std::max(zs, round_up(zsum, 128));
+    }
+    *xs_bytes = xs;
+    *zs_bytes = zs;
+    const size_t fixed = 1024 + xs + zs + kRingStages * (128 + 16) + 128;
+    const size_t kMaxSmem = 227 * 1024;
+    if (fixed + 2 * item > kMaxSmem) return 0;  // need >= 2 stages in flight
+    size_t ch = (kMaxSmem - fixed) / kRingStages / 128 * 128;
+    return std::max(ch, round_up(item, 128));
+}
+
+static bool chain_ok(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, bool mlp) {
+    size_t a, b;
+    return chain_chunk_bytes(wdt, phases, mlp, &a, &b) != 0;
+}
+
+// Single-launch decode chain (decode.cu).  phases[0] = linears sharing x; when
+// mlp is set, phase 0 is {up, gate} with the silu epilogue into act and phase
+// 1 is {down} reading act.
 static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, const void* x,
                       bool mlp, void* act, pg_dtype ydt, cudaStream_t st) {
     const size_t accs = wdt == PG_F64 ? 8 : 4, es = dtype_size(wdt);
     ChainParams P = {};
     P.nphase = (int)phases.size();
-    P.prefetch = 1;
-    size_t zbytes = 256, smem = 16;
-    std::vector<int> splits;
-    for (auto& ph : phases) {
-        int tot = 0;
-        for (auto& l : ph) tot += l.cap;
-        splits.push_back(chain_split(tot));
-        size_t zs = 0;
-        for (auto& l : ph) {
-            zbytes += round_up((size_t)l.cap * splits.back() * accs, 256);
-            zs += round_up(l.cap, 4) * accs;
-        }
-        smem = std::max({smem, (size_t)ph[0].n * es + 16, zs});
-    }
+    size_t xs_bytes = 0, zs_bytes = 0;
+    const size_t ch = chain_chunk_bytes(wdt, phases, mlp, &xs_bytes, &zs_bytes);
+    if (!ch) throw Error{PG_INVALID_ARGUMENT, "decode chain: operands exceed shared memory"};
+    P.xs_bytes = (int)xs_bytes;
+    P.zs_bytes = (int)zs_bytes;
+    P.chunk_bytes = (int)ch;
+    static const int stages_env = [] {
+        const char* e = getenv("PG_CHAIN_STAGES");
+        return e ? std::max(2, std::min(atoi(e), kRingStages)) : kRingStages;
+    }();
+    P.max_stages = stages_env;
+    P.dbg = chain_debug_buffer();
+    size_t zbytes = 256;
+    for (auto& ph : phases)
+        for (auto& l : ph) zbytes += round_up((size_t)l.cap * accs, 256);
     const size_t act_bytes = (mlp && !act) ? round_up((size_t)phases[0][0].m * es, 256) : 0;
-    Scratch ws(zbytes + act_bytes, st);
-    char* base = ws.as<char>();
-    PG_CUDA_THROW(cudaMemsetAsync(base, 0, 8, st));
+    // Persistent per-stream workspace: the grid-barrier counter is monotone
+    // (every launch adds a multiple of the grid size), so consecutive chain
+    // launches need no memset between them and can overlap under
+    // programmatic dependent launch.
+    char* base = chain_workspace(st, zbytes + act_bytes);
     P.bar = reinterpret_cast<unsigned long long*>(base);
     size_t off = 256;
     if (act_bytes) act = base + zbytes;
     for (size_t p = 0; p < phases.size(); ++p) {
         ChainPhase& Q = P.ph[p];
         Q.nlin = (int)phases[p].size();
-        Q.split = splits[p];
         Q.x = p == 0 ? x : act;
         Q.epilogue = (mlp && p == 0) ? 1 : 0;
         Q.ydt = ydt;
@@ -548,11 +626,11 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
             L.bt = S.bt; L.ldb = S.ldb; L.a = S.a; L.lda = S.lda; L.sm = S.sm; L.cap = S.cap;
             L.n = S.n; L.m = S.m; L.y = S.y;
             L.zpart = base + off;
-            off += round_up((size_t)S.cap * Q.split * accs, 256);
+            off += round_up((size_t)S.cap * accs, 256);
         }
     }
-    if (smem > 200 * 1024) throw Error{PG_INVALID_ARGUMENT, "decode chain: operands exceed shared memory"};
-    launch_chain(wdt, P, smem, st);
+    const size_t total = 1024 + xs_bytes + zs_bytes + kRingStages * (128 + 16) + 128 + (size_t)kRingStages * ch;
+    launch_chain(wdt, P, std::min(total, (size_t)227 * 1024), st);
 }
 
 static void run_forward(pg_dtype wdt, const void* bt, int64_t ldb, const void* a, int64_t lda,
@@ -560,9 +638,12 @@ static void run_forward(pg_dtype wdt, const void* bt, int64_t ldb, const void* a
                         void* y, pg_dtype ydt, cudaStream_t st) {
     if (T == 0) return;
     const size_t accs = wdt == PG_F64 ? 8 : 4;
-    if (T == 1 && (size_t)n * dtype_size(wdt) <= 190 * 1024 && (size_t)nslots_max * accs <= 190 * 1024) {
-        run_chain(wdt, {{LinSpec{bt, ldb, a, lda, sm, nslots_max, n, m, y}}}, x, false, nullptr, ydt, st);
-        return;
+    if (T == 1) {
+        std::vector<std::vector<LinSpec>> ph = {{LinSpec{bt, ldb, a, lda, sm, nslots_max, n, m, y}}};
+        if (chain_ok(wdt, ph, false)) {
+            run_chain(wdt, ph, x, false, nullptr, ydt, st);
+            return;
+        }
     }
     if (decode_tmax(T) && decode_smem_need(wdt, n, nslots_max, T) <= 200 * 1024) {
         Scratch z((size_t)nslots_max * T * accs, st);
@@ -851,7 +932,13 @@ int pg_module_forward(const pg_agg* gs, size_t nlin, const size_t* patterns, con
         check_ydt(gs[l]->dt, ydt);
         ph.push_back(agg_spec(gs[l], pattern_dev ? 0 : (int)patterns[l], pattern_dev, ys[l]));
     }
-    run_chain(gs[0]->dt, {ph}, x, false, nullptr, ydt, as_stream(s));
+    const cudaStream_t st = as_stream(s);
+    if (chain_ok(gs[0]->dt, {ph}, false)) {
+        run_chain(gs[0]->dt, {ph}, x, false, nullptr, ydt, st);
+    } else {  // operands too wide for one launch: one chain per linear
+        for (const LinSpec& L : ph) run_forward(gs[0]->dt, L.bt, L.ldb, L.a, L.lda, L.sm, L.cap, L.n, L.m, x, 0, 1,
+                                                L.y, ydt, st);
+    }
     PG_API_END
 }
 
@@ -865,10 +952,34 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, 
     check_ydt(down->dt, ydt);
     const int p0 = pattern_dev ? 0 : (int)patterns[0], p1 = pattern_dev ? 0 : (int)patterns[1],
               p2 = pattern_dev ? 0 : (int)patterns[2];
-    run_chain(up->dt,
-              {{agg_spec(up, p0, pattern_dev, nullptr), agg_spec(gate, p1, pattern_dev, nullptr)},
-               {agg_spec(down, p2, pattern_dev, y)}},
-              x, true, act, ydt, as_stream(s));
+    const cudaStream_t st = as_stream(s);
+    const std::vector<std::vector<LinSpec>> ph = {
+        {agg_spec(up, p0, pattern_dev, nullptr), agg_spec(gate, p1, pattern_dev, nullptr)},
+        {agg_spec(down, p2, pattern_dev, y)}};
+    if (chain_ok(up->dt, ph, true)) {
+        run_chain(up->dt, ph, x, true, act, ydt, st);
+    } else {  // too wide for one launch: up, gate, silu, down as separate chains
+        const size_t accs = up->dt == PG_F64 ? 8 : 4, es = dtype_size(up->dt);
+        const pg_dtype mid = up->dt == PG_F64 ? PG_F64 : PG_F32;
+        Scratch ws(2 * round_up((size_t)up->m * accs, 256) + ((act == nullptr) ? (size_t)up->m * es : 0), st);
+        char* u = ws.as<char>();
+        char* g = u + round_up((size_t)up->m * accs, 256);
+        void* a = act ? act : (void*)(g + round_up((size_t)up->m * accs, 256));
+        for (int l = 0; l < 2; ++l) {
+            const LinSpec& L = ph[0][l];
+            run_forward(up->dt, L.bt, L.ldb, L.a, L.lda, L.sm, L.cap, L.n, L.m, x, 0, 1, l ? g : u, mid, st);
+        }
+        launch_silu_mul(g, u, mid, (size_t)up->m, a, up->dt, st);
+        const LinSpec& D = ph[1][0];
+        run_forward(up->dt, D.bt, D.ldb, D.a, D.lda, D.sm, D.cap, D.n, D.m, a, 0, 1, y, ydt, st);
+    }
+    PG_API_END
+}
+
+int pg_chain_debug_dump(uint64_t* out_host, size_t n) {
+    PG_API_BEGIN
+    require(out_host && g_chain_dbg, PG_INVALID_ARGUMENT, "chain debug: set PG_CHAIN_DBG=1");
+    PG_CUDA_THROW(cudaMemcpy(out_host, g_chain_dbg, std::min<size_t>(n, 1024 * 16) * 8, cudaMemcpyDeviceToHost));
     PG_API_END
 }
 

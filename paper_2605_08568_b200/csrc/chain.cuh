@@ -7,40 +7,45 @@ namespace pg {
 
 constexpr int kChainThreads = 512;
 constexpr int kChainWarps = kChainThreads / 32;
+constexpr int kConsumerWarps = kChainWarps - 1;  // warp 15 is the TMA producer
 constexpr int kMaxLin = 3;
 constexpr int kMaxPhase = 2;
+constexpr int kRingStages = 8;
+constexpr int kMaxChunkItems = 16;
 
 struct ChainLin {
-    const void* bt;
+    const void* bt;  // B^T arena [.., ldb] (storage dtype)
     int64_t ldb;
-    const void* a;
+    const void* a;   // A arena [m, lda]
     int64_t lda;
-    SlotMap sm;
-    int cap;      // slots upper bound (smem / partial sizing)
+    SlotMap sm;      // runs + activity mask (no gather lists), resolved on device
+    int cap;         // slots upper bound
     int n, m;
-    void* zpart;  // [cap * split] accumulator partials
-    void* y;      // output (epilogue 0)
+    void* zpart;     // [cap] accumulator-precision z (global exchange between CTAs)
+    void* y;         // output (epilogue 0)
 };
 
 struct ChainPhase {
     int nlin;
     ChainLin lin[kMaxLin];
-    const void* x;  // [n] input shared by the phase's linears (W dtype)
-    int epilogue;   // 0: y_l per linear (ydt); 1: act = silu(y_1) * y_0 -> act (W dtype)
+    const void* x;  // [n] phase input (storage dtype); phase 1 reads the phase-0 act
+    int epilogue;   // 0: y_l per linear (ydt); 1: act = silu(y_1) * y_0 -> act (storage dtype)
     int ydt;
     void* act;
-    int split;      // warps per slot row in stage 1
 };
 
 struct ChainParams {
     int nphase;
     ChainPhase ph[kMaxPhase];
-    unsigned long long* bar;
-    int prefetch;
+    unsigned long long* bar;  // grid-barrier counter (zeroed per launch)
+    int xs_bytes;             // shared-memory x region (max over phases)
+    int zs_bytes;             // shared-memory z region (max over phases)
+    int chunk_bytes;          // ring stage size
+    int max_stages;           // ring depth cap (<= kRingStages)
+    unsigned long long* dbg;  // optional per-CTA %globaltimer stamps [grid][16]
 };
 
 void launch_chain(pg_dtype wdt, const ChainParams& P, size_t smem, cudaStream_t st);
 int chain_grid();
-int chain_split(int total_slots);
 
 }  // namespace pg

@@ -4,17 +4,18 @@
 // MLP's silu(gate)*up (toy_lm.hpp:250-257) as a stage-2 epilogue feeding the
 // next phase (down_proj).
 //
-// One persistent cooperative kernel, one CTA per SM (148 x 512 threads):
-//   0. every CTA issues cp.async.bulk.prefetch.L2 for its 1/G share of ALL
-//      weight bytes the chain will read, so HBM streams at full rate from the
-//      first cycle and the later stages hit L2;
-//   1. stage 1: warp items (linear, slot, row-chunk) -> z partials (f32 acc);
-//   2. grid barrier; z (+ activity mask) into shared memory;
-//   3. stage 2: warps own output rows, A_S row runs dotted with z from smem;
-//   4. grid barrier before the next phase consumes this phase's output.
+// One persistent cooperative kernel, one CTA per SM, warp-specialised:
+//   * warp 15 (one elected thread) is the TMA producer: it walks this CTA's
+//     share of every weight row the chain reads -- stage-1 B^T rows of its slot
+//     range, then stage-2 A rows of its output-row range, phase by phase --
+//     and streams them with cp.async.bulk into a shared-memory ring
+//     (full/empty mbarriers).  Weight rows never depend on activations, so the
+//     producer keeps HBM busy straight through the grid barriers;
+//   * warps 0-14 consume chunks in order: stage 1 dots B^T rows with x (in
+//     smem) and publishes z; a grid barrier; z into smem; stage 2 dots A_S rows
+//     with z and writes y (or act = silu(gate)*up for the MLP, then phase 1).
 // Roofline: HBM-bound, algorithmic bytes = sum_l K_l (m_l + n_l) * dtype.
-// Deterministic: every reduction has a fixed order (warp trees, partials
-// summed in chunk order).
+// Deterministic: fixed reduction orders (warp trees) and fixed CTA ranges.
 #include <algorithm>
 
 #include "chain.cuh"
@@ -45,243 +46,496 @@ __device__ __forceinline__ void cunpack(const int4& v, A* o) {
     }
 }
 
-__device__ __forceinline__ int c_slot_index(const SlotMap& sm, int s) {
-    if (sm.idx) return sm.idx[s];
-    return s < sm.run0_len ? s : sm.run1_start + (s - sm.run0_len);
-}
-__device__ __forceinline__ bool c_slot_active(const SlotMap& sm, int s) {
-    if (sm.idx) return sm.idx[s] >= 0;
-    if (s < sm.run0_len) return sm.mask == nullptr || sm.mask[s] != 0;
-    return true;
-}
+// ---- shared-memory tables ----
+struct LinS {
+    const char* bt;
+    const char* a;
+    const uint8_t* mask;  // run0 activity (nullable)
+    void* z;
+    void* y;
+    long long ldb_b, lda_b;  // row strides (bytes)
+    int run0, run1_start, run1, nslots;
+    int n, m;
+    int s0, s1;  // this CTA's stage-1 slot range
+    int i0, i1;  // this CTA's stage-2 row range
+    int pad[2];
+};
+struct Desc {
+    int seg, lin, count, gidx, last;
+    int ids[kMaxChunkItems];
+    int pad[11];
+};
+static_assert(sizeof(Desc) == 128, "Desc layout");
 
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// ---- PTX helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// one LDS.128 (the compiler otherwise splits int4 views of bf16 data into
+// four 4-way-conflicted LDS.32)
+__device__ __forceinline__ int4 lds128(const void* p) {
+    int4 r;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(smem_u32(p)));
+    return r;
 }
-
-// prefetch [base, base+bytes) split over the grid; lanes of warp 0 issue 16 KB pieces
-__device__ void prefetch_range(const char* base, size_t bytes, int cta, int ncta, int lane) {
-    if (!base || bytes == 0) return;
-    const size_t per = ((bytes + ncta - 1) / ncta + 15) & ~size_t(15);
-    const size_t b0 = (size_t)cta * per;
-    if (b0 >= bytes) return;
-    const size_t b1 = min(bytes, b0 + per);
-    for (size_t o = b0 + (size_t)lane * 16384; o < b1; o += 32 * 16384) {
-        const size_t left = b1 - o;
-        const uint32_t len = (uint32_t)(left < 16384 ? left : 16384) & ~15u;
-        if (len) l2_prefetch(base + o, len);
-    }
+__device__ __forceinline__ float4 lds128f(const void* p) {
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(smem_u32(p)));
+    return r;
 }
-
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {  // named barrier over the 15 consumer warps
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define STAMP(k) \
+    if (P.dbg && threadIdx.x == 0) P.dbg[blockIdx.x * 16 + (k)] = gtimer()
 
-// Monotone counter barrier: each arrival adds 1; generation g completes when
-// the counter reaches (g+1)*G.  Requires co-residency (cooperative launch).
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar) {
-    __syncthreads();
+// Grid-wide barrier among consumer warps (the producer never blocks on it).
+// Monotone counter: generation g completes when the count reaches (g+1)*G.
+// The CTA barrier orders every consumer's z/act stores before thread 0's
+// release-add (release is cumulative), and the acquire poll orders the
+// subsequent reads -- no MEMBAR.GPU, which would also wait for the SM's
+// in-flight bulk copies.
+__device__ __forceinline__ void grid_sync_consumers(unsigned long long* bar) {
+    consumer_sync();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned long long old = atomicAdd(bar, 1ull);
+        unsigned long long old;
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
         const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
-        while (ld_acquire(bar) < target) __nanosleep(20);
-        __threadfence();
+        while (ld_acquire(bar) < target) {
+        }
     }
-    __syncthreads();
+    consumer_sync();
 }
 
-template <typename W>
-__device__ void chain_prefetch(const ChainParams& P, int lane) {
-    const int cta = blockIdx.x, ncta = gridDim.x;
-    const size_t es = sizeof(W);
-    for (int ph = 0; ph < P.nphase; ++ph) {
-        for (int l = 0; l < P.ph[ph].nlin; ++l) {
-            const ChainLin& L = P.ph[ph].lin[l];
-            const SlotMap sm = resolve(L.sm);
-            const char* bt = static_cast<const char*>(L.bt);
-            const char* a = static_cast<const char*>(L.a);
-            if (sm.idx) continue;  // gather layouts: no contiguous ranges to prefetch
-            prefetch_range(bt, (size_t)sm.run0_len * L.ldb * es, cta, ncta, lane);
-            prefetch_range(bt + (size_t)sm.run1_start * L.ldb * es, (size_t)sm.run1_len * L.ldb * es, cta,
-                           ncta, lane);
-            if (sm.run1_len == 0 && L.lda == sm.run0_len) {
-                prefetch_range(a, (size_t)L.m * L.lda * es, cta, ncta, lane);
-            } else {
-                for (int i = cta * 32 + lane; i < L.m; i += ncta * 32) {
-                    const char* row = a + (size_t)i * L.lda * es;
-                    if (sm.run0_len) l2_prefetch(row, (uint32_t)(sm.run0_len * es));
-                    if (sm.run1_len) l2_prefetch(row + (size_t)sm.run1_start * es, (uint32_t)(sm.run1_len * es));
-                }
-            }
+// Copy `count` elements global -> shared with every thread's loads issued
+// before any store (one latency instead of one per loop trip).
+template <typename T, int B>
+__device__ __forceinline__ void stage_batched(T* dst, const T* __restrict__ src, int count, int tid, int nthr) {
+    for (int base = 0; base < count; base += B * nthr) {
+        T v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int e = base + u * nthr + tid;
+            if (e < count) v[u] = src[e];
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int e = base + u * nthr + tid;
+            if (e < count) dst[e] = v[u];
         }
     }
 }
 
+// z value t of 16-byte weight vector v: bf16 uses the two-plane layout (see
+// the z staging), f32/f64 the plain one; the compiler fuses these into
+// vector LDS.
+template <int V, typename A>
+__device__ __forceinline__ A zv(const A* z, int pl, int v, int t) {
+    if constexpr (V == 8) return t < 4 ? z[v * 4 + t] : z[pl + v * 4 + (t - 4)];
+    else return z[v * V + t];
+}
+
+// acc += dot(16-byte weight vector v, matching z values), z loads as 16-byte LDS
+template <typename W, typename A>
+__device__ __forceinline__ A zdot(const int4& wraw, const A* z, int pl, int v, A acc) {
+    constexpr int V = CVec<W>::n;
+    A wv[V];
+    cunpack<W, A>(wraw, wv);
+    if constexpr (V == 8) {
+        const float4 lo = lds128f(z + v * 4);
+        const float4 hi = lds128f(z + pl + v * 4);
+        acc = fma(wv[0], lo.x, acc); acc = fma(wv[1], lo.y, acc);
+        acc = fma(wv[2], lo.z, acc); acc = fma(wv[3], lo.w, acc);
+        acc = fma(wv[4], hi.x, acc); acc = fma(wv[5], hi.y, acc);
+        acc = fma(wv[6], hi.z, acc); acc = fma(wv[7], hi.w, acc);
+    } else if constexpr (V == 4) {
+        const float4 q = lds128f(z + v * 4);
+        acc = fma(wv[0], q.x, acc); acc = fma(wv[1], q.y, acc);
+        acc = fma(wv[2], q.z, acc); acc = fma(wv[3], q.w, acc);
+    } else {
+        const double2 q = *reinterpret_cast<const double2*>(z + v * 2);
+        acc = fma(wv[0], q.x, acc); acc = fma(wv[1], q.y, acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ bool slot_on(const LinS& L, int s) {
+    return s >= L.run0 || L.mask == nullptr || L.mask[s] != 0;
+}
+__device__ __forceinline__ int slot_row(const LinS& L, int s) {
+    return s < L.run0 ? s : L.run1_start + (s - L.run0);
+}
+
+// ---------------------------------------------------------------- producer
+template <typename W>
+__device__ void chain_producer(const ChainParams& P, const LinS* lins, Desc* descs, uint64_t* full,
+                               uint64_t* empty, unsigned char* ring, int nst) {
+    constexpr int es = sizeof(W);
+    const int CH = P.chunk_bytes;
+    int k = 0;
+    unsigned uses = 0;      // parity of the next empty-wait per stage (bit k)
+    unsigned used_once = 0;
+    int gidx = 0;
+    int c_used = 0, c_cnt = 0;
+    Desc* d = nullptr;
+    auto open = [&](int seg, int lin) {
+        if (used_once & (1u << k)) {
+            mbar_wait(smem_u32(&empty[k]), (uses >> k) & 1u);
+            uses ^= 1u << k;
+        }
+        used_once |= 1u << k;
+        d = &descs[k];
+        d->seg = seg;
+        d->lin = lin;
+        d->gidx = gidx;
+        d->last = 0;
+        c_used = 0;
+        c_cnt = 0;
+    };
+    auto close = [&](int last) {
+        d->count = c_cnt;
+        d->last = last;
+        gidx += c_cnt;
+        mbar_arrive(smem_u32(&full[k]));
+        k = (k + 1 == nst) ? 0 : k + 1;
+        d = nullptr;
+    };
+    auto copy = [&](const char* src, int bytes) {
+        const uint32_t bar = smem_u32(&full[k]);
+        mbar_expect_tx(bar, (uint32_t)bytes);
+        bulk_g2s(smem_u32(ring + (size_t)k * CH + c_used), src, (uint32_t)bytes, bar);
+        c_used += bytes;
+    };
+    for (int ph = 0; ph < P.nphase; ++ph) {
+        const ChainPhase& Q = P.ph[ph];
+        const LinS* L = lins + ph * kMaxLin;
+        // ---- stage-1 segment: B^T rows of this CTA's slot range.  Slots of one
+        // run are consecutive B^T rows, so a chunk is ONE bulk copy; masked slots
+        // ride along and are zeroed when z is staged.
+        for (int l = 0; l < Q.nlin; ++l) {
+            const int rb = (int)L[l].ldb_b;
+            const int per = max(1, min(kMaxChunkItems, CH / rb));
+            int s = L[l].s0;
+            while (s < L[l].s1) {
+                // stay inside one run so the rows are contiguous
+                const int run_end = s < L[l].run0 ? min(L[l].s1, L[l].run0) : L[l].s1;
+                const int cnt = min(per, run_end - s);
+                open(2 * ph, l);
+                for (int q = 0; q < cnt; ++q) d->ids[q] = s + q;
+                c_cnt = cnt;
+                copy(L[l].bt + (size_t)slot_row(L[l], s) * L[l].ldb_b, cnt * rb);
+                s += cnt;
+                close(0);
+            }
+        }
+        open(2 * ph, 0);
+        close(1);
+        // ---- stage-2 segment: A_S rows of this CTA's row range.  Single-run
+        // arenas (lda == nslots) are contiguous: one copy per matrix per chunk.
+        if (Q.epilogue == 1) {
+            const int rb0 = L[0].nslots * es, rb1 = L[1].nslots * es;
+            const bool contig = L[0].run1 == 0 && L[1].run1 == 0 && L[0].lda_b == rb0 && L[1].lda_b == rb1;
+            const int per = max(1, min(kMaxChunkItems, CH / (rb0 + rb1)));
+            for (int i = L[0].i0; i < L[0].i1;) {
+                const int cnt = min(per, L[0].i1 - i);
+                open(2 * ph + 1, 0);
+                for (int q = 0; q < cnt; ++q) d->ids[q] = i + q;
+                c_cnt = cnt;
+                for (int l = 0; l < 2; ++l) {
+                    if (contig) {
+                        copy(L[l].a + (size_t)i * L[l].lda_b, cnt * (l ? rb1 : rb0));
+                    } else {
+                        for (int q = 0; q < cnt; ++q) {
+                            const char* row = L[l].a + (size_t)(i + q) * L[l].lda_b;
+                            copy(row, L[l].run0 * es);
+                            if (L[l].run1) copy(row + (size_t)L[l].run1_start * es, L[l].run1 * es);
+                        }
+                    }
+                }
+                i += cnt;
+                close(0);
+            }
+        } else {
+            for (int l = 0; l < Q.nlin; ++l) {
+                const int rb = L[l].nslots * es;
+                const bool contig = L[l].run1 == 0 && L[l].lda_b == rb;
+                const int per = max(1, min(kMaxChunkItems, CH / rb));
+                for (int i = L[l].i0; i < L[l].i1;) {
+                    const int cnt = min(per, L[l].i1 - i);
+                    open(2 * ph + 1, l);
+                    for (int q = 0; q < cnt; ++q) d->ids[q] = i + q;
+                    c_cnt = cnt;
+                    if (contig) {
+                        copy(L[l].a + (size_t)i * L[l].lda_b, cnt * rb);
+                    } else {
+                        for (int q = 0; q < cnt; ++q) {
+                            const char* row = L[l].a + (size_t)(i + q) * L[l].lda_b;
+                            copy(row, L[l].run0 * es);
+                            if (L[l].run1) copy(row + (size_t)L[l].run1_start * es, L[l].run1 * es);
+                        }
+                    }
+                    i += cnt;
+                    close(0);
+                }
+            }
+        }
+        open(2 * ph + 1, 0);
+        close(1);
+    }
+}
+
+// ---------------------------------------------------------------- kernel
 template <typename W>
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constant__ ChainParams P) {
     using A = typename Acc<W>::type;
     constexpr int V = CVec<W>::n;
-    constexpr int U = 8;  // 16-byte loads in flight per lane per batch
-    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int es = sizeof(W);
+    extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kChainWarps + warp, nw = gridDim.x * kChainWarps;
+    const int G = gridDim.x, c = blockIdx.x;
 
-    if (P.prefetch && warp == 0) chain_prefetch<W>(P, lane);
+    // ---- carve shared memory: [tables 1K][x][z][descs][full][empty][ring]
+    LinS* lins = reinterpret_cast<LinS*>(smem);
+    W* xs = reinterpret_cast<W*>(smem + 1024);
+    A* zs = reinterpret_cast<A*>(smem + 1024 + P.xs_bytes);
+    Desc* descs = reinterpret_cast<Desc*>(smem + 1024 + P.xs_bytes + P.zs_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(descs + kRingStages);
+    uint64_t* empty = full + kRingStages;
+    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char*>(empty + kRingStages) - smem) + 127) & ~size_t(127);
+    unsigned char* ring = smem + ring_off;
+    const int nst = (int)min((size_t)min(P.max_stages, kRingStages), (size_t)(227 * 1024 - ring_off) / (size_t)P.chunk_bytes);
 
+    STAMP(0);
+    if (threadIdx.x < P.nphase * kMaxLin) {
+        const int ph = threadIdx.x / kMaxLin, l = threadIdx.x % kMaxLin;
+        const ChainPhase& Q = P.ph[ph];
+        if (l < Q.nlin) {
+            const ChainLin& C = Q.lin[l];
+            const SlotMap sm = resolve(C.sm);
+            LinS& L = lins[threadIdx.x];
+            L.bt = static_cast<const char*>(C.bt);
+            L.a = static_cast<const char*>(C.a);
+            L.mask = sm.mask;
+            L.z = C.zpart;
+            L.y = C.y;
+            L.ldb_b = C.ldb * es;
+            L.lda_b = C.lda * es;
+            L.run0 = sm.run0_len;
+            L.run1_start = sm.run1_start;
+            L.run1 = sm.run1_len;
+            L.nslots = sm.run0_len + sm.run1_len;
+            L.n = C.n;
+            L.m = C.m;
+            L.s0 = (int)((long long)L.nslots * c / G);
+            L.s1 = (int)((long long)L.nslots * (c + 1) / G);
+            L.i0 = (int)((long long)C.m * c / G);
+            L.i1 = (int)((long long)C.m * (c + 1) / G);
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kRingStages; ++k) {
+            mbar_init(smem_u32(&full[k]), 1);
+            mbar_init(smem_u32(&empty[k]), kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // Let the next launch in the stream start its prologue / weight stream as
+    // soon as SMs free up (programmatic dependent launch).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp == kConsumerWarps) {
+        // weights are immutable: the producer never waits on the previous grid
+        if (lane == 0) chain_producer<W>(P, lins, descs, full, empty, ring, nst);
+        return;
+    }
+    // consumers read x and write z / act / y: wait for the previous grid
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    // ---- consumers
+    const int tid = threadIdx.x, nct = kConsumerWarps * 32;
+    int k = 0;
+    unsigned par = 0;  // full-barrier parity per stage
     for (int ph = 0; ph < P.nphase; ++ph) {
         const ChainPhase& Q = P.ph[ph];
-        const int n = Q.lin[0].n;
-        // ---- stage the phase input x into shared memory
-        W* xs = reinterpret_cast<W*>(smem);
+        const LinS* L = lins + ph * kMaxLin;
+        const int nlin = Q.nlin;
+        // stage x (phase 0: the input; phase 1: act, complete after the barrier)
         {
-            const int nv = (n * (int)sizeof(W)) / 16;
-            const int4* xv = reinterpret_cast<const int4*>(Q.x);
-            for (int v = threadIdx.x; v < nv; v += kChainThreads) reinterpret_cast<int4*>(xs)[v] = xv[v];
-            for (int e = nv * 16 / (int)sizeof(W) + threadIdx.x; e < n; e += kChainThreads)
-                xs[e] = static_cast<const W*>(Q.x)[e];
+            const int n = L[0].n;
+            const int nbytes = n * es;
+            stage_batched<int4, 4>(reinterpret_cast<int4*>(xs), reinterpret_cast<const int4*>(Q.x), nbytes / 16,
+                                   tid, nct);
+            for (int e = (nbytes / 16) * 16 / es + tid; e < n; e += nct) xs[e] = static_cast<const W*>(Q.x)[e];
+            for (int e = n + tid; e < (n + V - 1) / V * V; e += nct) xs[e] = W(0);
         }
-        __syncthreads();
-        // ---- stage 1: items (linear, slot, chunk)
-        const int split = Q.split;
-        int nsl[kMaxLin];
-        int total = 0;
-        for (int l = 0; l < Q.nlin; ++l) {
-            nsl[l] = resolve(Q.lin[l].sm).nslots();
-            total += nsl[l] * split;
-        }
-        const int nvec = n / V;
-        const int cvec = (nvec + split - 1) / split;
-        for (int it = gw; it < total; it += nw) {
-            int l = 0, rem = it;
-            while (l + 1 < Q.nlin && rem >= nsl[l] * split) { rem -= nsl[l] * split; ++l; }
-            const ChainLin& L = Q.lin[l];
-            const SlotMap sm = resolve(L.sm);
-            const int slot = rem / split, part = rem % split;
-            A acc = A(0);
-            if (c_slot_active(sm, slot)) {
-                const int4* row = reinterpret_cast<const int4*>(static_cast<const W*>(L.bt) +
-                                                                (int64_t)c_slot_index(sm, slot) * L.ldb);
-                const int v0 = part * cvec, v1 = min(nvec, v0 + cvec);
-                for (int vb = v0 + lane; vb < v1; vb += 32 * U) {
-                    int4 w4[U];
+        consumer_sync();
+        STAMP(ph * 6 + 1);
+        // ---- stage 1: z_s = B^T[s] . x
+        for (;;) {
+            mbar_wait(smem_u32(&full[k]), (par >> k) & 1u);
+            par ^= 1u << k;
+            const Desc& D = descs[k];
+            const int cnt = D.count, g0 = D.gidx, last = D.last, l = D.lin;
+            if (cnt) {
+                const LinS& Ls = L[l];
+                const int rb = (int)Ls.ldb_b;
+                const int nv = (Ls.n + V - 1) / V;
+                const unsigned char* base = ring + (size_t)k * P.chunk_bytes;
+                for (int q = (warp - g0 % kConsumerWarps + kConsumerWarps) % kConsumerWarps; q < cnt;
+                     q += kConsumerWarps) {
+                    const int4* rv = reinterpret_cast<const int4*>(base + (size_t)q * rb);
+                    const int4* xv = reinterpret_cast<const int4*>(xs);
+                    A acc = A(0);
+#pragma unroll 4
+                    for (int v = lane; v < nv; v += 32) {
+                        A wv[V], xx[V];
+                        cunpack<W, A>(lds128(rv + v), wv);
+                        cunpack<W, A>(lds128(xv + v), xx);
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (vb + 32 * u < v1) w4[u] = ld_stream(row + vb + 32 * u);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int v = vb + 32 * u;
-                        if (v < v1) {
-                            A wv[V], xv[V];
-                            cunpack<W, A>(w4[u], wv);
-                            cunpack<W, A>(*reinterpret_cast<const int4*>(xs + (int64_t)v * V), xv);
-#pragma unroll
-                            for (int q = 0; q < V; ++q) acc = fma(wv[q], xv[q], acc);
-                        }
+                        for (int t = 0; t < V; ++t) acc = fma(wv[t], xx[t], acc);
                     }
-                }
-                if (part == split - 1) {  // scalar tail when n % V != 0
-                    const W* rs = reinterpret_cast<const W*>(row);
-                    for (int j = nvec * V + lane; j < n; j += 32) {
-                        if constexpr (sizeof(W) == 2) acc = fma(__bfloat162float(rs[j]), __bfloat162float(xs[j]), acc);
-                        else acc = fma((A)rs[j], (A)xs[j], acc);
+                    acc = warp_sum(acc);
+                    if (lane == 0) {
+                        const int s = D.ids[q];  // masked slots publish 0 (exec_engine.hpp:221-223)
+                        static_cast<A*>(Ls.z)[s] = slot_on(Ls, s) ? acc : A(0);
                     }
                 }
             }
-            acc = warp_sum(acc);
-            if (lane == 0) static_cast<A*>(L.zpart)[(int64_t)slot * split + part] = acc;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&empty[k]));
+            k = (k + 1 == nst) ? 0 : k + 1;
+            if (last) break;
         }
-        grid_barrier(P.bar);
-        // ---- z into shared memory (partials summed in chunk order; mask)
-        A* zs = reinterpret_cast<A*>(smem);
+        STAMP(ph * 6 + 2);
+        grid_sync_consumers(P.bar);
+        STAMP(ph * 6 + 3);
+        // ---- z into shared memory (inactive slots -> 0)
         int zoff[kMaxLin];
         {
             int o = 0;
-            for (int l = 0; l < Q.nlin; ++l) {
+            for (int l = 0; l < nlin; ++l) {
                 zoff[l] = o;
-                const SlotMap sm = resolve(Q.lin[l].sm);
-                const A* zp = static_cast<const A*>(Q.lin[l].zpart);
-                for (int s = threadIdx.x; s < nsl[l]; s += kChainThreads) {
-                    A v = A(0);
-                    for (int q = 0; q < split; ++q) v += zp[(int64_t)s * split + q];
-                    zs[o + s] = c_slot_active(sm, s) ? v : A(0);
-                }
-                o += (nsl[l] + 3) & ~3;
-            }
-        }
-        __syncthreads();
-        // ---- stage 2: rows
-        const int rows_per_lin = Q.lin[0].m;
-        int row_total = 0;
-        if (Q.epilogue == 1) row_total = rows_per_lin;
-        else
-            for (int l = 0; l < Q.nlin; ++l) row_total += Q.lin[l].m;
-        for (int it = gw; it < row_total; it += nw) {
-            int l0 = 0, i = it;
-            if (Q.epilogue == 0)
-                while (l0 + 1 < Q.nlin && i >= Q.lin[l0].m) { i -= Q.lin[l0].m; ++l0; }
-            const int lcount = Q.epilogue == 1 ? 2 : 1;
-            A res[2] = {A(0), A(0)};
+                const A* z = static_cast<const A*>(L[l].z);
+                const int ns = L[l].nslots;
+                // inactive slots were already written as 0 by stage 1; loads are
+                // batched so each thread pays one L2 round trip, not one per slot
+                constexpr int B = 8;
+                const int pl = (ns + 7) / 8 * 4;
+                for (int base = 0; base < ns; base += B * nct) {
+                    A v[B];
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (k >= lcount) break;
-                const int l = Q.epilogue == 1 ? k : l0;
-                const ChainLin& L = Q.lin[l];
-                const SlotMap sm = resolve(L.sm);
-                const W* row = static_cast<const W*>(L.a) + (int64_t)i * L.lda;
-                const A* z = zs + zoff[l];
-                A acc = A(0);
-                if (sm.idx) {
-                    for (int s = lane; s < nsl[l]; s += 32) {
-                        const int c = sm.idx[s];
-                        if (c < 0) continue;
-                        if constexpr (sizeof(W) == 2) acc = fma(__bfloat162float(row[c]), z[s], acc);
-                        else acc = fma((A)row[c], z[s], acc);
+                    for (int u = 0; u < B; ++u) {
+                        const int s = base + u * nct + tid;
+                        if (s < ns) v[u] = z[s];
                     }
-                } else {
-                    const int nv0 = sm.run0_len / V, nv = nv0 + sm.run1_len / V;
-                    for (int vb = lane; vb < nv; vb += 32 * U) {
-                        int4 w4[U];
 #pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const int v = vb + 32 * u;
-                            if (v < nv) {
-                                const int col = v < nv0 ? v * V : sm.run1_start + (v - nv0) * V;
-                                w4[u] = ld_stream(row + col);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const int v = vb + 32 * u;
-                            if (v < nv) {
-                                A wv[V];
-                                cunpack<W, A>(w4[u], wv);
-#pragma unroll
-                                for (int q = 0; q < V; ++q) acc = fma(wv[q], z[v * V + q], acc);
-                            }
+                    for (int u = 0; u < B; ++u) {
+                        const int s = base + u * nct + tid;
+                        if (s < ns) {
+                            // bf16: two planes (slots 0-3 / 4-7 of every 8) so each
+                            // lane's 8 z-values are two conflict-free 16-byte loads
+                            if constexpr (V == 8) zs[o + (s >> 3) * 4 + (s & 3) + ((s & 4) ? pl : 0)] = v[u];
+                            else zs[o + s] = v[u];
                         }
                     }
                 }
-                res[k] = warp_sum(acc);
-            }
-            if (lane == 0) {
-                if (Q.epilogue == 1) {
-                    const float up = (float)res[0], g = (float)res[1];
-                    const float v = g / (1.0f + __expf(-g)) * up;
-                    W* act = static_cast<W*>(Q.act);
-                    if constexpr (sizeof(W) == 2) act[i] = __float2bfloat16_rn(v);
-                    else act[i] = (W)(g / (1.0f + expf(-g)) * up);
-                } else {
-                    void* y = Q.lin[l0].y;
-                    if (Q.ydt == PG_F32) static_cast<float*>(y)[i] = (float)res[0];
-                    else if (Q.ydt == PG_F64) static_cast<double*>(y)[i] = (double)res[0];
-                    else static_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn((float)res[0]);
-                }
+                o += (V == 8) ? 2 * pl : ((ns + 3) & ~3);
             }
         }
-        if (ph + 1 < P.nphase) grid_barrier(P.bar);
+        consumer_sync();
+        STAMP(ph * 6 + 4);
+        // ---- stage 2: y_i = A_S[i] . z
+        for (;;) {
+            mbar_wait(smem_u32(&full[k]), (par >> k) & 1u);
+            par ^= 1u << k;
+            const Desc& D = descs[k];
+            const int cnt = D.count, g0 = D.gidx, last = D.last, l = D.lin;
+            if (cnt) {
+                const unsigned char* base = ring + (size_t)k * P.chunk_bytes;
+                for (int q = (warp - g0 % kConsumerWarps + kConsumerWarps) % kConsumerWarps; q < cnt;
+                     q += kConsumerWarps) {
+                    const int i = D.ids[q];
+                    if (Q.epilogue == 1) {
+                        const int ns0 = L[0].nslots, ns1 = L[1].nslots;
+                        const int4* r0 = reinterpret_cast<const int4*>(base + (size_t)q * ns0 * es);
+                        const int4* r1 = reinterpret_cast<const int4*>(base + (size_t)cnt * ns0 * es + (size_t)q * ns1 * es);
+                        const A* z0 = zs + zoff[0];
+                        const A* z1 = zs + zoff[1];
+                        const int pl0 = (ns0 + 7) / 8 * 4, pl1 = (ns1 + 7) / 8 * 4;
+                        A a0 = A(0), a1 = A(0);
+                        for (int v = lane; v < ns0 / V; v += 32) {
+                            a0 = zdot<W, A>(lds128(r0 + v), z0, pl0, v, a0);
+                        }
+                        for (int v = lane; v < ns1 / V; v += 32) {
+                            a1 = zdot<W, A>(lds128(r1 + v), z1, pl1, v, a1);
+                        }
+                        a0 = warp_sum(a0);
+                        a1 = warp_sum(a1);
+                        if (lane == 0) {
+                            W* act = static_cast<W*>(Q.act);
+                            if constexpr (sizeof(W) == 2) {
+                                const float up = (float)a0, g = (float)a1;
+                                act[i] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * up);
+                            } else {
+                                act[i] = (W)(a1 / (A(1) + exp(-a1)) * a0);
+                            }
+                        }
+                    } else {
+                        const int ns = L[l].nslots;
+                        const int4* r = reinterpret_cast<const int4*>(base + (size_t)q * ns * es);
+                        const A* z = zs + zoff[l];
+                        const int pl = (ns + 7) / 8 * 4;
+                        A acc = A(0);
+                        for (int v = lane; v < ns / V; v += 32) {
+                            acc = zdot<W, A>(lds128(r + v), z, pl, v, acc);
+                        }
+                        acc = warp_sum(acc);
+                        if (lane == 0) {
+                            void* y = L[l].y;
+                            if (Q.ydt == PG_F32) static_cast<float*>(y)[i] = (float)acc;
+                            else if (Q.ydt == PG_F64) static_cast<double*>(y)[i] = (double)acc;
+                            else static_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn((float)acc);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&empty[k]));
+            k = (k + 1 == nst) ? 0 : k + 1;
+            if (last) break;
+        }
+        STAMP(ph * 6 + 5);
+        if (ph + 1 < P.nphase) grid_sync_consumers(P.bar);  // act complete before phase ph+1 reads it
     }
 }
 
@@ -295,17 +549,11 @@ int chain_grid() {
     return g_num_sms;
 }
 
-int chain_split(int total_slots) {
-    const int nw = chain_grid() * kChainWarps;
-    int s = (nw + total_slots - 1) / std::max(total_slots, 1);
-    return std::max(1, std::min(s, 8));
-}
-
 template <typename W>
 static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_chain<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_chain<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -313,11 +561,28 @@ static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st) {
     cfg.blockDim = dim3(kChainThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    static const int coop = [] {
+        const char* e = getenv("PG_CHAIN_COOP");
+        return e ? atoi(e) : 1;
+    }();
+    static const int pdl = [] {
+        const char* e = getenv("PG_CHAIN_PDL");
+        return e ? atoi(e) : 1;
+    }();
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    if (pdl) {  // programmatic dependent launch: the producer may start streaming
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_chain<W>, P));
     count_launch();
 }
