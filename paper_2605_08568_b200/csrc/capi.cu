@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "chain.cuh"
+#include "umma.cuh"
 
 namespace pg {
 
@@ -55,6 +56,7 @@ void launch_fill_normal(void* out, pg_dtype dt, size_t count, uint64_t seed, dou
                         cudaStream_t st);
 void launch_silu_mul(const void* g, const void* u, pg_dtype in_dt, size_t count, void* act,
                      pg_dtype act_dt, cudaStream_t st);
+void launch_transpose(pg_dtype dt, const void* src, int rows, int cols, void* dst, cudaStream_t st);
 
 // ---- stream-ordered scratch (freed when the scope ends, after queued work) ----
 static void init_pool() {
@@ -633,6 +635,86 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
     launch_chain(wdt, P, std::min(total, (size_t)227 * 1024), st);
 }
 
+// ---- bf16 prefill on the tensor cores (umma.cu): stage 1 and stage 2 of every
+// job are one grouped launch each.  Jobs whose slot map has a second run or an
+// activity mask are first gathered into a contiguous [ns] arena (masked slots
+// become zero rows, so their z is exactly 0).
+struct PrefillJob {
+    const void* bt;
+    int64_t ldb;
+    const void* a;
+    int64_t lda;
+    SlotMap sm;
+    int n, m;
+    const void* x;  // token-major [T, n] bf16
+    int T;
+    void* y;        // token-major [T, m]
+    pg_dtype ydt;
+};
+
+static bool prefill_ok(int n, int T) { return T > 8 && n % 8 == 0; }
+
+static void run_prefill(const std::vector<PrefillJob>& jobs, cudaStream_t st) {
+    const size_t es = 2;
+    // workspace: packed operands (when needed) + Z per job
+    std::vector<size_t> zoff(jobs.size()), poff(jobs.size(), (size_t)-1);
+    size_t bytes = 0;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+        const PrefillJob& J = jobs[j];
+        const int ns = J.sm.nslots();
+        const bool pack = J.sm.idx || J.sm.run1_len || J.sm.mask;
+        if (pack) {
+            poff[j] = bytes;
+            bytes += round_up((size_t)ns * 4, 256) + round_up((size_t)ns * J.ldb * es, 256) +
+                     round_up((size_t)J.m * ns * es, 256);
+        }
+        zoff[j] = bytes;
+        bytes += round_up((size_t)J.T * ns * es, 256);
+    }
+    Scratch ws(bytes, st);
+    char* base = ws.as<char>();
+    std::vector<UmmaSpec> s1, s2;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+        const PrefillJob& J = jobs[j];
+        const int ns = J.sm.nslots();
+        const void* bt = J.bt;
+        const void* a = J.a;
+        int64_t lda = J.lda;
+        if (poff[j] != (size_t)-1) {
+            // gather list over the slot map: -1 for inactive (masked) slots
+            std::vector<int32_t> idx(ns);
+            if (J.sm.idx) {
+                PG_CUDA_THROW(cudaMemcpyAsync(idx.data(), J.sm.idx, ns * 4, cudaMemcpyDeviceToHost, st));
+                PG_CUDA_THROW(cudaStreamSynchronize(st));
+            } else {
+                std::vector<uint8_t> mask(J.sm.run0_len, 1);
+                if (J.sm.mask) {
+                    PG_CUDA_THROW(cudaMemcpyAsync(mask.data(), J.sm.mask, J.sm.run0_len, cudaMemcpyDeviceToHost, st));
+                    PG_CUDA_THROW(cudaStreamSynchronize(st));
+                }
+                for (int s = 0; s < ns; ++s)
+                    idx[s] = s < J.sm.run0_len ? (mask[s] ? s : -1) : J.sm.run1_start + (s - J.sm.run0_len);
+            }
+            char* p = base + poff[j];
+            int32_t* didx = reinterpret_cast<int32_t*>(p);
+            void* pb = p + round_up((size_t)ns * 4, 256);
+            void* pa = static_cast<char*>(pb) + round_up((size_t)ns * J.ldb * es, 256);
+            PG_CUDA_THROW(cudaMemcpyAsync(didx, idx.data(), ns * 4, cudaMemcpyHostToDevice, st));
+            PG_CUDA_THROW(cudaStreamSynchronize(st));  // idx is host-owned
+            launch_gather_rows(PG_BF16, J.bt, J.ldb, didx, ns, ns, J.n, pb, J.ldb, st);
+            launch_gather_cols(PG_BF16, J.a, J.lda, didx, ns, ns, J.m, pa, ns, st);
+            bt = pb;
+            a = pa;
+            lda = ns;
+        }
+        void* z = base + zoff[j];
+        s1.push_back(UmmaSpec{J.x, J.n, bt, J.ldb, z, ns, J.T, ns, J.n, 1});
+        s2.push_back(UmmaSpec{z, ns, a, lda, J.y, J.m, J.T, J.m, ns, J.ydt == PG_BF16 ? 1 : 0});
+    }
+    launch_umma(s1, st);
+    launch_umma(s2, st);
+}
+
 static void run_forward(pg_dtype wdt, const void* bt, int64_t ldb, const void* a, int64_t lda,
                         SlotMap sm, int nslots_max, int n, int m, const void* x, int fm, int T,
                         void* y, pg_dtype ydt, cudaStream_t st) {
@@ -644,6 +726,20 @@ static void run_forward(pg_dtype wdt, const void* bt, int64_t ldb, const void* a
             run_chain(wdt, ph, x, false, nullptr, ydt, st);
             return;
         }
+    }
+    if (wdt == PG_BF16 && prefill_ok(n, T) && !sm.dyn_pattern) {
+        // tensor-core prefill; feature-major operands are transposed around it
+        const void* xt = x;
+        void* yt = y;
+        Scratch tx(fm ? (size_t)T * n * 2 : 0, st), ty(fm ? (size_t)T * m * dtype_size(ydt) : 0, st);
+        if (fm) {
+            launch_transpose(PG_BF16, x, n, T, tx.p, st);  // [n, T] -> [T, n]
+            xt = tx.p;
+            yt = ty.p;
+        }
+        run_prefill({PrefillJob{bt, ldb, a, lda, sm, n, m, xt, T, yt, ydt}}, st);
+        if (fm) launch_transpose(ydt, ty.p, T, m, y, st);  // [T, m] -> [m, T]
+        return;
     }
     if (decode_tmax(T) && decode_smem_need(wdt, n, nslots_max, T) <= 200 * 1024) {
         Scratch z((size_t)nslots_max * T * accs, st);
@@ -878,16 +974,23 @@ int pg_aggregated_forward_batched(pg_agg g, const int32_t* pats, const int64_t* 
     check_ydt(g->dt, ydt);
     const cudaStream_t st = as_stream(s);
     const size_t es = dtype_size(g->dt), ys = dtype_size(ydt);
+    std::vector<PrefillJob> jobs;  // bf16 prompts with T > 8: one grouped tensor-core launch per stage
     for (size_t q = 0; q < P; ++q) {
         const int p = pats[q];
         if (p < 0 || p >= g->P) throw Error{PG_OUT_OF_RANGE, "unknown pattern"};
         const int64_t t0 = offs[q], t1 = offs[q + 1];
         if (t1 <= t0) continue;
         SlotMap sm = agg_slotmap(g, p);
-        run_forward(g->dt, g->bt_arena, g->ldb, g->a_arena, g->lda, sm, sm.nslots(), g->n, g->m,
-                    static_cast<const char*>(x) + t0 * g->n * es, 0, (int)(t1 - t0),
-                    static_cast<char*>(y) + t0 * g->m * ys, ydt, st);
+        const void* xq = static_cast<const char*>(x) + t0 * g->n * es;
+        void* yq = static_cast<char*>(y) + t0 * g->m * ys;
+        if (g->dt == PG_BF16 && prefill_ok(g->n, (int)(t1 - t0))) {
+            jobs.push_back(PrefillJob{g->bt_arena, g->ldb, g->a_arena, g->lda, sm, g->n, g->m, xq, (int)(t1 - t0), yq, ydt});
+            continue;
+        }
+        run_forward(g->dt, g->bt_arena, g->ldb, g->a_arena, g->lda, sm, sm.nslots(), g->n, g->m, xq, 0,
+                    (int)(t1 - t0), yq, ydt, st);
     }
+    if (!jobs.empty()) run_prefill(jobs, st);
     PG_API_END
 }
 

@@ -1,0 +1,331 @@
+// umma.cu -- K5: grouped bf16 GEMM on the 5th-gen tensor cores (tcgen05 + TMEM
+// + TMA) for prefill, i.e. T > 8 tokens through a rank-expert layer:
+//   stage 1  Z[T, Kp] = X[T, n]  . B_S^T[Kp, n]^T   (both operands K-major)
+//   stage 2  Y[T, m]  = Z[T, Kp] . A_S [m, Kp]^T    (both operands K-major)
+// (rank_experts.hpp:52-72 / exec_engine.hpp:193-236 at large T).  A "group" is
+// one GEMM; heterogeneous prompts (each with its own S) are one launch.
+//
+// Persistent, warp-specialised, one CTA per SM (192 threads):
+//   warp 0      TMA producer: 128x64 A box + BNx64 B box per k-block, 128B
+//               swizzle, 4-stage smem ring (full/empty mbarriers);
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::f16, bf16 x bf16 -> f32, M=128, N=BN<=256, K=16),
+//               double-buffered accumulators (2 x 256 TMEM columns);
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> registers -> bf16/f32 ->
+//               global (row/column masked), then release the accumulator.
+// Roofline: tensor-pipe-bound, 2*M*N*K flops per group.
+#include <cuda.h>
+
+#include <algorithm>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "umma.cuh"
+
+namespace pg {
+
+constexpr int UM_BM = 128, UM_BK = 64, UM_BN_MAX = 256, UM_STAGES = 4;
+constexpr int UM_THREADS = 192;
+constexpr int UM_A_BYTES = UM_BM * UM_BK * 2;          // 16 KB
+constexpr int UM_B_BYTES = UM_BN_MAX * UM_BK * 2;      // 32 KB (max)
+constexpr int UM_STAGE_BYTES = UM_A_BYTES + UM_B_BYTES;
+constexpr int UM_SMEM = UM_STAGES * UM_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+constexpr int UM_MAX_GROUPS = 32;
+
+struct UmmaGroup {
+    void* out;                 // [M, ldo] row-major
+    long long ldo;
+    int M, N, K;
+    int bn;                    // tile N (multiple of 16, <= 256)
+    int out_bf16;              // 1: bf16 out, 0: f32 out
+    int tiles_m, tiles_n;
+    int tile_base;             // prefix sum of tiles over groups
+};
+
+// Passed as one __grid_constant__ parameter block (< 32 KB): TMA reads the
+// tensor maps straight from parameter space, no staging copy.
+struct __align__(64) UmmaParams {
+    CUtensorMap maps[2 * UM_MAX_GROUPS];  // [2g] A [M rows, K] box {64,128}; [2g+1] B [N rows, K] box {64,BN}
+    UmmaGroup groups[UM_MAX_GROUPS];
+    int ngroups;
+    int total_tiles;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t u_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void u_mbar_init(uint32_t b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c) : "memory");
+}
+__device__ __forceinline__ void u_mbar_wait(uint32_t b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(b),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void u_mbar_arrive_tx(uint32_t b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void u_mbar_arrive(uint32_t b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void u_tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t u_desc(uint32_t saddr) {
+    // K-major, 128B swizzle: LBO=1 (unused), SBO=1024B, version 1 (sm100), layout 2
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void u_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void u_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_constant__ UmmaParams P) {
+    extern __shared__ __align__(1024) unsigned char usmem[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(usmem) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + UM_STAGES * UM_STAGE_BYTES);
+    uint64_t* full = bars;                     // [STAGES]
+    uint64_t* empty = bars + UM_STAGES;        // [STAGES]
+    uint64_t* tfull = bars + 2 * UM_STAGES;    // [2]
+    uint64_t* tempty = bars + 2 * UM_STAGES + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * UM_STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < UM_STAGES; ++s) {
+            u_mbar_init(u_smem(&full[s]), 1);
+            u_mbar_init(u_smem(&empty[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            u_mbar_init(u_smem(&tfull[a]), 1);
+            u_mbar_init(u_smem(&tempty[a]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // allocate all 512 TMEM columns (2 accumulators x 256)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(u_smem(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+                int g = 0;
+                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+                const UmmaGroup& G = P.groups[g];
+                const int lt = t - G.tile_base;
+                const int m0 = (lt % G.tiles_m) * UM_BM, n0 = (lt / G.tiles_m) * G.bn;
+                const int kbs = (G.K + UM_BK - 1) / UM_BK;
+                const uint32_t bytes = UM_A_BYTES + (uint32_t)G.bn * UM_BK * 2;
+                for (int kb = 0; kb < kbs; ++kb) {
+                    u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
+                    const uint32_t fb = u_smem(&full[s]);
+                    u_mbar_arrive_tx(fb, bytes);
+                    unsigned char* st = base + s * UM_STAGE_BYTES;
+                    u_tma_2d(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
+                    u_tma_2d(u_smem(st + UM_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
+                    if (++s == UM_STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int s = 0, acc = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+                int g = 0;
+                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+                const UmmaGroup& G = P.groups[g];
+                const int kbs = (G.K + UM_BK - 1) / UM_BK;
+                const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(G.bn >> 3) << 17) |
+                                       ((uint32_t)(UM_BM >> 4) << 24);
+                u_mbar_wait(u_smem(&tempty[acc]), aph ^ 1);  // epilogue drained this accumulator
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(acc * UM_BN_MAX);
+                for (int kb = 0; kb < kbs; ++kb) {
+                    u_mbar_wait(u_smem(&full[s]), ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = u_smem(base + s * UM_STAGE_BYTES), sb = sa + UM_A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < UM_BK / 16; ++k)
+                        u_mma(d, u_desc(sa + k * 32), u_desc(sb + k * 32), idesc, (kb | k) != 0);
+                    u_commit(u_smem(&empty[s]));  // frees the smem stage when these MMAs retire
+                    if (++s == UM_STAGES) { s = 0; ph ^= 1; }
+                }
+                u_commit(u_smem(&tfull[acc]));  // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; aph ^= 1; }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2-5)
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+            int g = 0;
+            while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+            const UmmaGroup& G = P.groups[g];
+            const int lt = t - G.tile_base;
+            const int m0 = (lt % G.tiles_m) * UM_BM, n0 = (lt / G.tiles_m) * G.bn;
+            u_mbar_wait(u_smem(&tfull[acc]), aph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int row = m0 + q * 32 + lane;
+            for (int c0 = 0; c0 < G.bn; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * UM_BN_MAX + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < G.M) {
+                    const int cb = n0 + c0;
+                    if (G.out_bf16) {
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(G.out) + (long long)row * G.ldo + cb;
+                        if (cb + 32 <= G.N && ((G.ldo & 7) == 0)) {
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                uint4 w;
+                                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
+                                                                             __uint_as_float(r[v * 8 + 2 * e + 1]));
+                                    wp[e] = *reinterpret_cast<uint32_t*>(&h);
+                                }
+                                *reinterpret_cast<uint4*>(o + v * 8) = w;
+                            }
+                        } else {
+                            for (int e = 0; e < 32 && cb + e < G.N; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+                        }
+                    } else {
+                        float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
+                        if (cb + 32 <= G.N && ((G.ldo & 3) == 0)) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v)
+                                *reinterpret_cast<float4*>(o + v * 4) =
+                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                        } else {
+                            for (int e = 0; e < 32 && cb + e < G.N; ++e) o[e] = __uint_as_float(r[e]);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) u_mbar_arrive(u_smem(&tempty[acc]));
+            if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    if (!fn) throw Error{PG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
+    return fn;
+}
+
+// 2-D bf16 K-major operand [rows, K] with row stride ld (elements), box {64, box_rows}
+static CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {UM_BK, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error{PG_CUDA_ERROR, "cuTensorMapEncodeTiled failed"};
+    return m;
+}
+
+static int pick_bn(int N) {
+    const int tiles = (N + UM_BN_MAX - 1) / UM_BN_MAX;
+    int bn = (N + tiles - 1) / tiles;
+    bn = (bn + 15) / 16 * 16;
+    return std::min(bn, UM_BN_MAX);
+}
+
+void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
+        attr = true;
+    }
+    int dev = 0, sms = 0;
+    PG_CUDA_THROW(cudaGetDevice(&dev));
+    PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (size_t g0 = 0; g0 < specs.size(); g0 += UM_MAX_GROUPS) {
+        const int ng = (int)std::min<size_t>(UM_MAX_GROUPS, specs.size() - g0);
+        auto P = std::make_unique<UmmaParams>();
+        int tiles = 0;
+        for (int g = 0; g < ng; ++g) {
+            const UmmaSpec& s = specs[g0 + g];
+            if ((s.lda * 2) % 16 || (s.ldb * 2) % 16 || s.K % 8)
+                throw Error{PG_INVALID_ARGUMENT, "umma: operands need 16-byte aligned rows"};
+            UmmaGroup& G = P->groups[g];
+            G.bn = pick_bn(s.N);
+            P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
+            P->maps[2 * g + 1] = make_map(s.b, s.N, s.K, s.ldb, G.bn);
+            G.out = s.out;
+            G.ldo = s.ldo;
+            G.M = s.M;
+            G.N = s.N;
+            G.K = s.K;
+            G.out_bf16 = s.out_bf16;
+            G.tiles_m = (s.M + UM_BM - 1) / UM_BM;
+            G.tiles_n = (s.N + G.bn - 1) / G.bn;
+            G.tile_base = tiles;
+            tiles += G.tiles_m * G.tiles_n;
+        }
+        P->ngroups = ng;
+        P->total_tiles = tiles;
+        if (tiles == 0) continue;
+        k_umma_grouped<<<std::min(tiles, sms), UM_THREADS, UM_SMEM, st>>>(*P);
+        PG_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace pg

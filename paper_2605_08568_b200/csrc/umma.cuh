@@ -1,0 +1,26 @@
+// umma.cuh -- host interface of the tcgen05 grouped GEMM (umma.cu).
+#pragma once
+
+#include <vector>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+// One GEMM C[M, N] = A[M, K] . B[N, K]^T, bf16 operands (both K-major, rows
+// 16-byte aligned), f32 accumulation, bf16 or f32 output.
+struct UmmaSpec {
+    const void* a;
+    long long lda;
+    const void* b;
+    long long ldb;
+    void* out;
+    long long ldo;
+    int M, N, K;
+    int out_bf16;
+};
+
+// All specs run as grouped launches (<= 32 groups per launch), async on st.
+void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st);
+
+}  // namespace pg

@@ -381,6 +381,31 @@ __global__ void k_silu_mul(const In* __restrict__ g, const In* __restrict__ u, s
     }
 }
 
+// dst[c, r] = src[r, c] (32x32 smem tiles)
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ src, int rows, int cols, T* __restrict__ dst) {
+    __shared__ T tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = src[(int64_t)r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) dst[(int64_t)c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+void launch_transpose(pg_dtype dt, const void* src, int rows, int cols, void* dst, cudaStream_t st) {
+    dim3 g((cols + 31) / 32, (rows + 31) / 32), b(32, 8);
+    if (dt == PG_F64) k_transpose<double><<<g, b, 0, st>>>(static_cast<const double*>(src), rows, cols, static_cast<double*>(dst));
+    else if (dt == PG_F32) k_transpose<float><<<g, b, 0, st>>>(static_cast<const float*>(src), rows, cols, static_cast<float*>(dst));
+    else k_transpose<__nv_bfloat16><<<g, b, 0, st>>>(static_cast<const __nv_bfloat16*>(src), rows, cols,
+                                                     static_cast<__nv_bfloat16*>(dst));
+    PG_LAUNCH_CHECK();
+}
+
 void launch_silu_mul(const void* g, const void* u, pg_dtype in_dt, size_t count, void* act,
                      pg_dtype act_dt, cudaStream_t st) {
     const int blocks = (int)std::min<size_t>((count + 255) / 256, kNumSMs * 4);

@@ -16,6 +16,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 TOL64, TOL32, TOLBF = 1e-10, 1e-5, 1e-4
+# bf16 prefill on the tensor cores (T > 8) rounds z to bf16 between the two GEMMs
+TOLBF_PREFILL = 8e-3
 
 
 @pytest.fixture(scope="module")
@@ -255,10 +257,10 @@ def test_masked_forward_bf16(pg, port, T):
     L = pg.FactorizedLayer(A, B, K, dtype="bf16")
     y = pg.masked_forward(L, pg.RankSelection(sel), torch.from_numpy(x).cuda().to(torch.bfloat16))
     assert y.dtype == torch.float32
-    assert rel(y.cpu().numpy(), ref) <= TOLBF
+    assert rel(y.cpu().numpy(), ref) <= (TOLBF if T <= 8 else TOLBF_PREFILL)
     yb = pg.masked_forward(L, pg.RankSelection(sel), torch.from_numpy(x).cuda().to(torch.bfloat16),
                            out_dtype=torch.bfloat16)
-    assert rel(yb.double().cpu().numpy(), ref) <= 8e-3
+    assert rel(yb.double().cpu().numpy(), ref) <= (8e-3 if T <= 8 else 1.2e-2)
 
 
 def test_check_selection_errors(pg, port):
@@ -319,7 +321,7 @@ def test_aggregated_forward_matches_masked(pg, port, dtype, T):
         A, B, x = bf16_round(A), bf16_round(B), bf16_round(x)
     elif dtype == "f32":
         A, B, x = (v.astype(np.float32).astype(np.float64) for v in (A, B, x))
-    tol = {"f64": TOL64, "f32": TOL32, "bf16": TOLBF}[dtype]
+    tol = {"f64": TOL64, "f32": TOL32, "bf16": TOLBF if T <= 8 else TOLBF_PREFILL}[dtype]
     for pid, sel in enumerate(pats):
         ref = port.masked_forward(A, B, sel, x)
         tr = pg.AccessTrace()

@@ -1,0 +1,86 @@
+"""K5: bf16 prefill on the tensor cores (tcgen05 + TMEM + TMA grouped GEMM).
+
+Two bars:
+  * GEMM mechanics vs a plain PyTorch fp32 reference of the SAME two GEMMs
+    (z rounded to bf16 between them, as the kernel does): max|d|/max|ref| <= 2e-3
+    (accumulation order only);
+  * end to end vs the f64 oracle on the same bf16-rounded A, B, X:
+    <= 8e-3 (TOLBF_PREFILL).
+Shapes cover ragged M (tokens), N not a multiple of the 256 tile (m=1000,
+K=832 -> 4 x 208), multi-pattern arenas (packing + masks) and grouped prompts.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_08568_b200 as m
+    return m
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def layer_data(port, m, n, r, seed):
+    sig = 1.0 / (1.0 + np.arange(r) / 64.0)
+    A = port.gaussian(seed, (m, r)) * sig / np.sqrt(m)
+    B = port.gaussian(seed + 1, (n, r)) / np.sqrt(n)
+    return A, B
+
+
+def torch_ref(A, B, sel, x_tok):
+    """fp32 reference of the kernel's math: z = bf16(x B_S), y = z A_S^T (token-major)."""
+    Ab = torch.from_numpy(A[:, sel]).to(torch.bfloat16).float().cuda()
+    Bb = torch.from_numpy(B[:, sel]).to(torch.bfloat16).float().cuda()
+    xb = x_tok.float()
+    z = (xb @ Bb).to(torch.bfloat16).float()
+    return (z @ Ab.t()).double().cpu().numpy()
+
+
+@pytest.mark.parametrize("m,n,r,K,T", [(1000, 4096, 1664, 832, 200), (4096, 4096, 1638, 819, 128),
+                                       (512, 1024, 384, 150, 37), (11008, 4096, 2388, 1194, 256)])
+def test_prefill_masked_forward(pg, port, m, n, r, K, T):
+    A, B = layer_data(port, m, n, r, 7 + m)
+    sel = port.select_topk(port.gaussian(8 + m, (r,)), K)
+    x = port.gaussian(9 + m, (T, n))
+    L = pg.FactorizedLayer(A, B, K, dtype="bf16")
+    xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    n0 = pg.launch_count()
+    y = pg.masked_forward(L, pg.RankSelection(sel), xt, layout="token")
+    assert pg.launch_count() > n0
+    assert rel(y.cpu().numpy(), torch_ref(A, B, sel, xt)) <= 2e-3
+    bfr = lambda a: torch.from_numpy(np.asarray(a)).to(torch.bfloat16).double().numpy()  # noqa: E731
+    ref = port.masked_forward(bfr(A), bfr(B), sel, bfr(x).T).T
+    assert rel(y.cpu().numpy(), ref) <= 8e-3
+    # feature-major activations (the reference's Mat layout) through the same kernel
+    yf = pg.masked_forward(L, pg.RankSelection(sel), xt.t().contiguous())
+    assert torch.equal(yf.t().contiguous(), y)
+
+
+def test_prefill_grouped_heterogeneous_prompts(pg, port):
+    """config-3 style: several prompts, each with its own expert subset, in one
+    grouped launch per stage; equals the per-prompt path bit for bit."""
+    m, n, r, K = 2048, 1024, 768, 384
+    A, B = layer_data(port, m, n, r, 3)
+    from oracle import pyoracle
+    pats = [p[0] for p in pyoracle.make_patterns(17171, 6, [(r, K)])]
+    L = pg.FactorizedLayer(A, B, K, dtype="bf16")
+    g = pg.aggregate_layout(L, [pg.RankSelection(p) for p in pats], 0.9)  # multi-pattern arena: masks + 2 runs
+    lens = [128, 300, 17, 64, 256, 9]
+    pids = [0, 3, 5, 1, 2, 4]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    X = torch.from_numpy(port.gaussian(4, (offs[-1], n))).cuda().to(torch.bfloat16)
+    Y = pg.aggregated_forward_batched(g, pids, offs, X)
+    for q, pid in enumerate(pids):
+        xq = X[offs[q]:offs[q + 1]].contiguous()
+        yq = pg.aggregated_forward(g, pid, xq, layout="token")
+        assert torch.equal(Y[offs[q]:offs[q + 1]], yq)
+        assert rel(yq.cpu().numpy(), torch_ref(A, B, pats[pid].astype(np.int64), xq)) <= 2e-3
