@@ -213,6 +213,13 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns_h
                    const int32_t* pattern_dev, const void* x_dev, void* act_dev, void* y_dev,
                    pg_dtype y_dtype, pg_stream stream);
 
+/* K5 primitive: C[M, N] = A[M, K] . B[N, K]^T on the tcgen05 tensor cores
+ * (bf16 operands, both K-major with 16-byte aligned rows, f32 accumulation;
+ * out bf16 when out_bf16 else f32).  The prefill paths are two of these per
+ * prompt, grouped across prompts. */
+int pg_gemm_bf16(const void* a_dev, int64_t lda, const void* b_dev, int64_t ldb, void* out_dev,
+                 int64_t ldo, size_t M, size_t N, size_t K, int out_bf16, pg_stream stream);
+
 /* MLP glue between upgate() and down_proj() (toy_lm.hpp:250-257):
  * act[i] = silu(gate[i]) * up[i], computed in f32 (f64 for f64 inputs) and
  * stored in act_dtype.  gate/up dtype in_dtype (PG_F32 or PG_F64). */

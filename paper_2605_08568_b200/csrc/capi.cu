@@ -1095,3 +1095,12 @@ int pg_fill_normal_device(void* out, pg_dtype dt, size_t count, uint64_t seed, d
 }
 
 }  // extern "C"
+
+extern "C" int pg_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, void* out, int64_t ldo, size_t M,
+                            size_t N, size_t K, int out_bf16, pg_stream s) {
+    PG_API_BEGIN
+    require(a && b && out, PG_INVALID_ARGUMENT, "gemm: null operand");
+    require(K % 8 == 0 && lda % 8 == 0 && ldb % 8 == 0, PG_INVALID_ARGUMENT, "gemm: rows must be 16-byte aligned");
+    launch_umma({UmmaSpec{a, lda, b, ldb, out, ldo, (int)M, (int)N, (int)K, out_bf16}}, as_stream(s));
+    PG_API_END
+}

@@ -205,9 +205,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (row < G.M) {
                     const int cb = n0 + c0;
+                    // columns of THIS tile only: the tile may be narrower than a 32-column chunk
+                    const int valid = min(32, min(G.bn - c0, G.N - cb));
                     if (G.out_bf16) {
                         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(G.out) + (long long)row * G.ldo + cb;
-                        if (cb + 32 <= G.N && ((G.ldo & 7) == 0)) {
+                        if (valid == 32 && ((G.ldo & 7) == 0)) {
 #pragma unroll
                             for (int v = 0; v < 4; ++v) {
                                 uint4 w;
@@ -221,18 +223,18 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
                                 *reinterpret_cast<uint4*>(o + v * 8) = w;
                             }
                         } else {
-                            for (int e = 0; e < 32 && cb + e < G.N; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+                            for (int e = 0; e < valid; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
                         }
                     } else {
                         float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
-                        if (cb + 32 <= G.N && ((G.ldo & 3) == 0)) {
+                        if (valid == 32 && ((G.ldo & 3) == 0)) {
 #pragma unroll
                             for (int v = 0; v < 8; ++v)
                                 *reinterpret_cast<float4*>(o + v * 4) =
                                     make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
                         } else {
-                            for (int e = 0; e < 32 && cb + e < G.N; ++e) o[e] = __uint_as_float(r[e]);
+                            for (int e = 0; e < valid; ++e) o[e] = __uint_as_float(r[e]);
                         }
                     }
                 }

@@ -84,3 +84,23 @@ def test_prefill_grouped_heterogeneous_prompts(pg, port):
         yq = pg.aggregated_forward(g, pid, xq, layout="token")
         assert torch.equal(Y[offs[q]:offs[q + 1]], yq)
         assert rel(yq.cpu().numpy(), torch_ref(A, B, pats[pid].astype(np.int64), xq)) <= 2e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 16, 16), (200, 1000, 832), (200, 832, 4096), (16, 832, 4096),
+                                   (1024, 1216, 4096), (300, 11008, 1216), (2048, 4096, 832)])
+def test_gemm_primitive_vs_torch(pg, M, N, K):
+    """pg_gemm_bf16 (the K5 building block) vs torch fp32 matmul of the same bf16
+    operands; covers ragged M, tiles narrower than 32-column chunks (N=832 ->
+    4 x 208) and long K loops around the 4-stage ring."""
+    from paper_2605_08568_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    for out_bf16 in (0, 1):
+        c = torch.full((M, N), float("nan"), device="cuda",
+                       dtype=torch.bfloat16 if out_bf16 else torch.float32)
+        _lib.call("pg_gemm_bf16", a.data_ptr(), K, b.data_ptr(), K, c.data_ptr(), N, M, N, K, out_bf16,
+                  torch.cuda.current_stream().cuda_stream)
+        ref = a.float() @ b.float().t()
+        err = ((c.float() - ref).abs().max() / ref.abs().max()).item()
+        assert err <= (8e-3 if out_bf16 else 1e-5), err
