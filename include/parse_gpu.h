@@ -213,6 +213,14 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns_h
                    const int32_t* pattern_dev, const void* x_dev, void* act_dev, void* y_dev,
                    pg_dtype y_dtype, pg_stream stream);
 
+/* Heterogeneous prefill (config 3): prompt p owns tokens
+ * [offsets_host[p], offsets_host[p+1]) of token-major x (bf16) and its own
+ * aggregated layout aggs[p] (served with pattern 0, e.g. the single pattern
+ * packed after routing / a cache hit).  All prompts' stage-1 GEMMs run as one
+ * grouped tcgen05 launch, then all stage-2 GEMMs.  y token-major. */
+int pg_prefill_batched(const pg_agg* aggs, const int64_t* offsets_host, size_t n_prompts,
+                       const void* x_dev, void* y_dev, pg_dtype y_dtype, pg_stream stream);
+
 /* K5 primitive: C[M, N] = A[M, K] . B[N, K]^T on the tcgen05 tensor cores
  * (bf16 operands, both K-major with 16-byte aligned rows, f32 accumulation;
  * out bf16 when out_bf16 else f32).  The prefill paths are two of these per

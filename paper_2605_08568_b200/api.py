@@ -520,6 +520,20 @@ def aggregated_forward_batched(agg: AggregatedLayer, pattern_ids, offsets, x: to
     return y
 
 
+def prefill_batched(aggs: list, offsets, x: torch.Tensor, out_dtype=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Heterogeneous bf16 prefill (config 3): prompt p (tokens offsets[p]:offsets[p+1]
+    of token-major x) is served by its own packed layout aggs[p]; all prompts run as
+    grouped tcgen05 GEMM launches."""
+    x = _dev(x, torch.bfloat16)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    ydt = _out_dtype(aggs[0].layer.dtype, out_dtype)
+    y = out if out is not None else torch.empty((x.shape[0], aggs[0].m), dtype=_TORCH[ydt], device=x.device)
+    hs = (C.c_void_p * len(aggs))(*[g.handle.value for g in aggs])
+    call("pg_prefill_batched", hs, offs.ctypes.data_as(C.POINTER(C.c_int64)), len(aggs), _ptr(x), _ptr(y), ydt,
+         _stream())
+    return y
+
+
 def scattered_forward(layer: FactorizedLayer, sel, x: torch.Tensor, trace: AccessTrace | None = None,
                       layout: str = "feature", out_dtype=None) -> torch.Tensor:
     """exec_engine.hpp:239-252: K strided column gathers in S order."""

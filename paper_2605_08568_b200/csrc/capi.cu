@@ -1104,3 +1104,32 @@ extern "C" int pg_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t l
     launch_umma({UmmaSpec{a, lda, b, ldb, out, ldo, (int)M, (int)N, (int)K, out_bf16}}, as_stream(s));
     PG_API_END
 }
+
+extern "C" int pg_prefill_batched(const pg_agg* aggs, const int64_t* offs, size_t P, const void* x, void* y,
+                                  pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(aggs && offs && x && y && P > 0, PG_INVALID_ARGUMENT, "prefill_batched: bad arguments");
+    const pg_agg g0 = aggs[0];
+    require(g0 && g0->dt == PG_BF16, PG_INVALID_ARGUMENT, "prefill_batched: bf16 layouts only");
+    check_ydt(g0->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const size_t ys = dtype_size(ydt);
+    std::vector<PrefillJob> jobs;
+    for (size_t q = 0; q < P; ++q) {
+        const pg_agg g = aggs[q];
+        require(g && g->dt == PG_BF16 && g->n == g0->n && g->m == g0->m, PG_INVALID_ARGUMENT,
+                "prefill_batched: layouts must share shape and dtype");
+        const int64_t t0 = offs[q], t1 = offs[q + 1];
+        if (t1 <= t0) continue;
+        const void* xq = static_cast<const char*>(x) + t0 * g->n * 2;
+        void* yq = static_cast<char*>(y) + t0 * g->m * ys;
+        SlotMap sm = agg_slotmap(g, 0);
+        if (prefill_ok(g->n, (int)(t1 - t0)))
+            jobs.push_back(PrefillJob{g->bt_arena, g->ldb, g->a_arena, g->lda, sm, g->n, g->m, xq, (int)(t1 - t0), yq, ydt});
+        else
+            run_forward(g->dt, g->bt_arena, g->ldb, g->a_arena, g->lda, sm, sm.nslots(), g->n, g->m, xq, 0,
+                        (int)(t1 - t0), yq, ydt, st);
+    }
+    if (!jobs.empty()) run_prefill(jobs, st);
+    PG_API_END
+}
