@@ -146,9 +146,12 @@ class RouterParams:
         self.handle = h
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.lib().pg_router_destroy(self.handle)
-            self.handle = None
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            try:
+                _lib.lib().pg_router_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
 
 
 def make_router(r: int, n: int, tau: float = 1.0, eps: float = 1e-8) -> RouterParams:
@@ -245,9 +248,12 @@ class PatternCache:
         self.handle = h
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.lib().pg_cache_destroy(self.handle)
-            self.handle = None
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            try:
+                _lib.lib().pg_cache_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
 
     def load(self, entries: list[CacheEntry]) -> None:
         """Bulk load (load_cache, pattern_cache.hpp:294-327)."""
@@ -357,9 +363,12 @@ class FactorizedLayer:
         return _TORCH[self.dtype]
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.lib().pg_layer_destroy(self.handle)
-            self.handle = None
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            try:
+                _lib.lib().pg_layer_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
 
 
 def _out_dtype(wdt: int, out_dtype):
@@ -468,9 +477,12 @@ class AggregatedLayer:
         return AccessTrace(list(c), list(c))
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.lib().pg_agg_destroy(self.handle)
-            self.handle = None
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            try:
+                _lib.lib().pg_agg_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
 
 
 def aggregate_layout(layer: FactorizedLayer, patterns, psi: float = 0.9) -> AggregatedLayer:
