@@ -152,6 +152,7 @@ struct pg_agg_s {
     void* a_arena;   // [m, lda] lda = arena_cols
     int64_t lda;
     uint8_t* masks;   // [P, s_pad]
+    std::vector<char> mask_full;  // pattern p uses every shared expert: no activity mask needed
     int32_t* table;   // [P, 2] (run1_start, run1_len)
     size_t bytes;
 };
@@ -841,8 +842,12 @@ int pg_aggregate_layout(pg_agg* out, pg_layer L, const uint32_t* pats, const siz
         for (size_t j = 0; j < g->res_ids[p].size(); ++j) idx[g->dev_off[p] + j] = (int32_t)g->res_ids[p][j];
     std::vector<uint8_t> masks((size_t)P * g->s_pad, 0);
     std::vector<int32_t> table(2 * P);
+    g->mask_full.assign(P, 1);
     for (size_t p = 0; p < P; ++p) {
-        for (size_t j = 0; j < sc; ++j) masks[p * g->s_pad + j] = g->use_shared[p][j];
+        for (size_t j = 0; j < sc; ++j) {
+            masks[p * g->s_pad + j] = g->use_shared[p][j];
+            if (!g->use_shared[p][j]) g->mask_full[p] = 0;
+        }
         table[2 * p] = g->dev_off[p];
         table[2 * p + 1] = g->cnt_pad[p];
     }
@@ -930,7 +935,9 @@ static SlotMap agg_slotmap(pg_agg g, int p) {
     sm.run0_len = g->s_pad;
     sm.run1_start = g->dev_off[p];
     sm.run1_len = g->cnt_pad[p];
-    sm.mask = g->masks + (size_t)p * g->s_pad;
+    // padding slots are zero rows / columns, so a pattern that uses every
+    // shared expert needs no activity mask
+    sm.mask = g->mask_full[p] ? nullptr : g->masks + (size_t)p * g->s_pad;
     return sm;
 }
 
