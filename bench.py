@@ -340,14 +340,19 @@ def prefill_arm(pg, torch, dev, world, P=16, T=2048):
         routers[nm] = pg.RouterParams(torch.randn((r, n), generator=g, device=dev, dtype=torch.float64))
         outs[nm] = torch.empty(P * T, m, device=dev, dtype=torch.bfloat16)
         flops += 2 * P * T * K * (m + n)
-    # routing (timed separately): select_topk(score(mean_pool(x_p))) per prompt, one launch set per router
+    # routing (timed separately): select_topk(score(mean_pool(x_p))) per prompt.
+    # Linears sharing an input pool it once (toy_lm.hpp:220-249: q/k/v and
+    # up/gate read hn, o the attention output, down act), then every router
+    # scores its own pooled input.
+    Xo = torch.randn(P * T, D_MODEL, device=dev, generator=g).to(torch.bfloat16)
+    src = {"q": X, "k": X, "v": X, "up": X, "gate": X, "o": Xo, "down": X2}
     sels = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for rep in range(2):
         e0.record()
+        pooled = {id(x): pg.mean_pool(x, layout="token", offsets=offs) for x in (X, Xo, X2)}
         for nm in lin:
-            sels[nm] = pg.route_select(routers[nm], X2 if nm == "down" else X, layers[nm][1], layout="token",
-                                       offsets=offs)
+            sels[nm] = pg.route_select_pooled(routers[nm], pooled[id(src[nm])], layers[nm][1])
         e1.record()
         torch.cuda.synchronize()
     route_ms = e0.elapsed_time(e1)
@@ -360,7 +365,7 @@ def prefill_arm(pg, torch, dev, world, P=16, T=2048):
 
     def layer_step():
         for nm in lin:
-            pg.prefill_batched(aggs[nm], offs, X2 if nm == "down" else X, out_dtype=torch.bfloat16, out=outs[nm])
+            pg.prefill_batched(aggs[nm], offs, src[nm], out_dtype=torch.bfloat16, out=outs[nm])
 
     for _ in range(2):
         layer_step()

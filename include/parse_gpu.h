@@ -92,6 +92,12 @@ int pg_route_select(pg_router router, const void* x_dev, pg_dtype x_dtype, pg_la
                     const int64_t* offsets_host, size_t n_prompts, size_t k, uint32_t* sel_dev,
                     double* logits_dev, pg_stream stream);
 
+/* The same routing step from already pooled inputs h_dev (n_prompts x n f64,
+ * mean_pool output): linears that share an input (q/k/v, up/gate,
+ * toy_lm.hpp:220-249) pool it once and route every router from it. */
+int pg_route_select_pooled(pg_router router, const double* h_dev, size_t n_prompts, size_t k,
+                           uint32_t* sel_dev, double* logits_dev, pg_stream stream);
+
 /* ------------------------------------------------------------------ */
 /* a9-a12: pattern cache  (pattern_cache.hpp:38-65,95-124)             */
 /* ------------------------------------------------------------------ */

@@ -50,6 +50,7 @@ _SIGS = {
     "pg_score": [_vp, _vp, _sz, _vp, _i, _vp],
     "pg_select_topk": [_vp, _sz, _sz, _sz, _vp, _vp],
     "pg_route_select": [_vp, _vp, _i, _i, _i64p, _sz, _sz, _vp, _vp, _vp],
+    "pg_route_select_pooled": [_vp, _vp, _sz, _sz, _vp, _vp, _vp],
     "pg_cosine": [_vp, _vp, _sz, _vp, _vp],
     "pg_cache_create": [C.POINTER(_vp), _sz, _sz, C.c_double],
     "pg_cache_destroy": [_vp],

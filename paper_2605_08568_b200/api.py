@@ -214,6 +214,23 @@ def route_select(router: RouterParams, x: torch.Tensor, k: int, layout: str = "f
     return (sel, lg) if return_logits else sel
 
 
+def route_select_pooled(router: RouterParams, h: torch.Tensor, k: int, return_logits: bool = False):
+    """route_select from already pooled inputs h (P x n f64 device, mean_pool's
+    output): linears sharing an input (q/k/v, up/gate; toy_lm.hpp:220-249) pool
+    once.  Bit-identical to route_select on the same x."""
+    h = _dev(h, torch.float64)
+    if h.dim() == 1:
+        h = h.unsqueeze(0)
+    if h.shape[-1] != router.n:
+        raise ValueError("score: bad input length")
+    P = h.shape[0]
+    sel = torch.empty((P, max(k, 1)), dtype=torch.int32, device=h.device)
+    lg = torch.empty((P, router.r), dtype=torch.float64, device=h.device) if return_logits else None
+    call("pg_route_select_pooled", router.handle, _ptr(h), P, k, _ptr(sel), _ptr(lg) if lg is not None else None,
+         _stream())
+    return (sel, lg) if return_logits else sel
+
+
 # ---------------------------------------------------------------- pattern cache
 @dataclass
 class PromptEmbedding:

@@ -24,7 +24,7 @@ void set_error(int code, const std::string& msg) {
 void launch_mean_pool(const void* x, pg_dtype dt, pg_layout lay, int n, int64_t ttot,
                       const int64_t* offs_dev, int P, double* h, cudaStream_t st);
 void launch_score(const double* theta, const double* bias, int r, int n, const double* h, int P,
-                  double* z, double* bnd, int exact, cudaStream_t st);
+                  double* z, double* bnd, int exact, cudaStream_t st, double* hnorm = nullptr);
 void launch_select_topk(const double* logits, int r, int P, int K, uint32_t* sel, cudaStream_t st);
 void launch_route_select(const double* zfast, const double* bnd, const double* theta,
                          const double* bias, const double* h, int r, int n, int K, int P,
@@ -247,8 +247,9 @@ int pg_router_destroy(pg_router R) {
 int pg_score(pg_router R, const double* h, size_t P, double* logits, int exact, pg_stream s) {
     PG_API_BEGIN
     require(R && h && logits && P > 0, PG_INVALID_ARGUMENT, "score: bad input length");
+    Scratch hn(exact ? 0 : P * 8, as_stream(s));
     launch_score(R->theta, R->bias, R->r, R->n, h, (int)P, logits, nullptr, exact ? 1 : 0,
-                 as_stream(s));
+                 as_stream(s), hn.as<double>());
     PG_API_END
 }
 
@@ -271,17 +272,37 @@ int pg_route_select(pg_router R, const void* x, pg_dtype dt, pg_layout lay, cons
     const size_t r = R->r, n = R->n;
     // sub-buffers 256-byte aligned (the GEMV reads h / theta with 16-byte loads)
     const size_t o_h = round_up((P + 1) * 8, 256), o_z = o_h + round_up(P * n * 8, 256),
-                 o_b = o_z + round_up(P * r * 8, 256);
-    Scratch ws(o_b + P * r * 8, st);
+                 o_b = o_z + round_up(P * r * 8, 256), o_n = o_b + round_up(P * r * 8, 256);
+    Scratch ws(o_n + P * 8, st);
     int64_t* od = ws.as<int64_t>();
     double* h = reinterpret_cast<double*>(ws.as<char>() + o_h);
     double* z = reinterpret_cast<double*>(ws.as<char>() + o_z);
     double* bnd = reinterpret_cast<double*>(ws.as<char>() + o_b);
     PG_CUDA_THROW(cudaMemcpyAsync(od, offs, (P + 1) * 8, cudaMemcpyHostToDevice, st));
     launch_mean_pool(x, dt, lay, (int)n, offs[P], od, (int)P, h, st);
-    launch_score(R->theta, R->bias, (int)r, (int)n, h, (int)P, z, bnd, 0, st);
+    launch_score(R->theta, R->bias, (int)r, (int)n, h, (int)P, z, bnd, 0, st,
+                 reinterpret_cast<double*>(ws.as<char>() + o_n));
     launch_route_select(z, bnd, R->theta, R->bias, h, (int)r, (int)n, (int)k, (int)P, sel,
                         logits_out, nullptr, st);
+    PG_API_END
+}
+
+int pg_route_select_pooled(pg_router R, const double* h, size_t P, size_t k, uint32_t* sel, double* logits_out,
+                           pg_stream s) {
+    PG_API_BEGIN
+    require(R && h && sel && P > 0, PG_INVALID_ARGUMENT, "route_select: bad arguments");
+    require(k != 0 && k <= (size_t)R->r, PG_INVALID_ARGUMENT, "select_topk: K out of range");
+    require(R->r <= max_select_rows(), PG_INVALID_ARGUMENT, "select_topk: too many experts for device top-k");
+    const cudaStream_t st = as_stream(s);
+    const size_t r = R->r, n = R->n;
+    const size_t o_b = round_up(P * r * 8, 256), o_n = o_b + round_up(P * r * 8, 256);
+    Scratch ws(o_n + P * 8, st);
+    double* z = ws.as<double>();
+    double* bnd = reinterpret_cast<double*>(ws.as<char>() + o_b);
+    launch_score(R->theta, R->bias, (int)r, (int)n, h, (int)P, z, bnd, 0, st,
+                 reinterpret_cast<double*>(ws.as<char>() + o_n));
+    launch_route_select(z, bnd, R->theta, R->bias, h, (int)r, (int)n, (int)k, (int)P, sel, logits_out, nullptr,
+                        st);
     PG_API_END
 }
 

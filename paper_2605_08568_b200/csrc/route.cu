@@ -23,16 +23,75 @@ namespace pg {
 
 // ---------------- mean_pool (router.hpp:80-88) ----------------
 
+// token-major x [Ttot, n]: one thread per (prompt, feature) sums its column in
+// token order; loads run kPoolAhead tokens ahead of the (strictly sequential)
+// fp64 additions so each thread keeps that many requests in flight.
+constexpr int kPoolAhead = 32;
 template <typename TX>
-__global__ void k_mean_pool_tm(const TX* __restrict__ x, int n, const int64_t* __restrict__ offs,
-                               double* __restrict__ h) {
+__global__ void __launch_bounds__(256) k_mean_pool_tm(const TX* __restrict__ x, int n,
+                                                      const int64_t* __restrict__ offs, double* __restrict__ h) {
     const int p = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t t0 = offs[p], t1 = offs[p + 1];
+    const TX* col = x + i;
     double s = 0.0;
-    for (int64_t t = t0; t < t1; ++t) s = __dadd_rn(s, to_d(x[t * (int64_t)n + i]));
+    int64_t t = t0;
+    for (; t + kPoolAhead <= t1; t += kPoolAhead) {
+        TX v[kPoolAhead];
+#pragma unroll
+        for (int u = 0; u < kPoolAhead; ++u) v[u] = col[(t + u) * (int64_t)n];
+#pragma unroll
+        for (int u = 0; u < kPoolAhead; ++u) s = __dadd_rn(s, to_d(v[u]));
+    }
+    for (; t < t1; ++t) s = __dadd_rn(s, to_d(col[t * (int64_t)n]));
     h[(int64_t)p * n + i] = __ddiv_rn(s, (double)(t1 - t0));
+}
+
+// bf16, n even: two features per thread (one 32-bit load per token feeds two
+// sequential chains); batches of kPoolAhead2 tokens are double-buffered in
+// registers, so the next batch's loads are in flight while this one's strictly
+// ordered fp64 additions run.
+constexpr int kPoolAhead2 = 64;
+__device__ __forceinline__ void pool_load(uint32_t (&v)[kPoolAhead2], const uint32_t* col, int64_t t, int64_t ld) {
+#pragma unroll
+    for (int u = 0; u < kPoolAhead2; ++u) v[u] = __ldg(col + (t + u) * ld);
+}
+__device__ __forceinline__ void pool_add(const uint32_t (&v)[kPoolAhead2], double& s0, double& s1) {
+#pragma unroll
+    for (int u = 0; u < kPoolAhead2; ++u) {
+        s0 = __dadd_rn(s0, (double)__uint_as_float(v[u] << 16));
+        s1 = __dadd_rn(s1, (double)__uint_as_float(v[u] & 0xffff0000u));
+    }
+}
+__global__ void __launch_bounds__(128) k_mean_pool_tm_bf16x2(const __nv_bfloat16* __restrict__ x, int n,
+                                                             const int64_t* __restrict__ offs,
+                                                             double* __restrict__ h) {
+    const int p = blockIdx.y;
+    const int i2 = blockIdx.x * blockDim.x + threadIdx.x;  // feature pair
+    if (2 * i2 >= n) return;
+    const int64_t t0 = offs[p], t1 = offs[p + 1];
+    const uint32_t* col = reinterpret_cast<const uint32_t*>(x) + i2;
+    const int64_t ld = n / 2;
+    double s0 = 0.0, s1 = 0.0;
+    const int64_t nb = (t1 - t0) / kPoolAhead2;  // whole batches
+    uint32_t va[kPoolAhead2], vb[kPoolAhead2];
+    if (nb > 0) pool_load(va, col, t0, ld);
+    for (int64_t b = 0; b < nb; b += 2) {
+        if (b + 1 < nb) pool_load(vb, col, t0 + (b + 1) * kPoolAhead2, ld);
+        pool_add(va, s0, s1);
+        if (b + 1 >= nb) break;
+        if (b + 2 < nb) pool_load(va, col, t0 + (b + 2) * kPoolAhead2, ld);
+        pool_add(vb, s0, s1);
+    }
+    for (int64_t t = t0 + nb * kPoolAhead2; t < t1; ++t) {
+        const uint32_t v = __ldg(col + t * ld);
+        s0 = __dadd_rn(s0, (double)__uint_as_float(v << 16));
+        s1 = __dadd_rn(s1, (double)__uint_as_float(v & 0xffff0000u));
+    }
+    const double T = (double)(t1 - t0);
+    h[(int64_t)p * n + 2 * i2] = __ddiv_rn(s0, T);
+    h[(int64_t)p * n + 2 * i2 + 1] = __ddiv_rn(s1, T);
 }
 
 // feature-major x [n, Ttot]: each warp owns 32 rows; a 32x32 tile is read
@@ -65,64 +124,99 @@ __global__ void k_mean_pool_fm(const TX* __restrict__ x, int n, int64_t ttot,
 
 // ---------------- score (router.hpp:41-46) ----------------
 
-constexpr int kScoreWarps = 8;
-constexpr int kScoreChunkP = 4;  // prompts per pass
 
-// fast: one warp per theta row, 16-byte loads, FMA tree; also the bound.
-__global__ void __launch_bounds__(kScoreWarps * 32)
+// ||h_p||_2 per prompt (rounded; inflated where it is used)
+__global__ void k_hnorm(const double* __restrict__ h, int n, double* __restrict__ out) {
+    __shared__ double red[32];
+    const double* hp = h + (int64_t)blockIdx.x * n;
+    double s = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) s = fma(hp[j], hp[j], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) out[blockIdx.x] = sqrt(v);
+    }
+}
+
+// fast: logits on the fp64 tensor cores (mma.m8n8k4.f64) plus a rigorous
+// error bound.  A block = kScoreSlices warps on 8 theta rows x 16 prompts,
+// warp s on the s-th slice of the reduction dimension; partial tiles are
+// summed across slices in fixed order.  Any summation order of the n products
+// is within gamma_{n+1} sum_j |theta_ij h_j| of the exact value (as is the
+// reference's sequential dot), and by Cauchy-Schwarz sum_j |theta_ij h_j| <=
+// ||theta_i|| ||h||, so
+//   bnd_i = 4 (n+2) u (||theta_i|| ||h|| + |b_i|)   (x 1.0000001 for the
+// rounding of the norms themselves) bounds |fast - reference|.
+constexpr int kScoreSlices = 8;
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(kScoreSlices * 32)
 k_score_fast(const double* __restrict__ theta, const double* __restrict__ bias, int r, int n,
-             const double* __restrict__ h, int P, double* __restrict__ z,
+             const double* __restrict__ h, const double* __restrict__ hnorm, int P, double* __restrict__ z,
              double* __restrict__ bnd) {
-    const int lane = threadIdx.x & 31;
-    const int row = blockIdx.x * kScoreWarps + (threadIdx.x >> 5);
-    if (row >= r) return;
+    __shared__ double part[kScoreSlices][32][5];  // per lane: 2 tiles x 2 + row-norm partial
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row0 = blockIdx.x * 8, p0 = blockIdx.y * 16;
+    const int rr = lane >> 2, cc = lane & 3;  // fragment row (theta row / prompt), k lane
+    const int row = min(row0 + rr, r - 1);
     const double* th = theta + (int64_t)row * n;
-    const double gam = 4.0 * (double)(n + 2) * kU;
-    const double tiny = 4.0 * (double)(n + 2) * 4.9406564584124654e-324;
-    for (int p0 = 0; p0 < P; p0 += kScoreChunkP) {
-        const int np = min(kScoreChunkP, P - p0);
-        double acc[kScoreChunkP], sab[kScoreChunkP];
-#pragma unroll
-        for (int q = 0; q < kScoreChunkP; ++q) acc[q] = sab[q] = 0.0;
-        const bool vec = ((n & 1) == 0);
-        if (vec) {
-            for (int j = 2 * lane; j < n; j += 64) {
-                const double2 t = __ldg(reinterpret_cast<const double2*>(th + j));
-#pragma unroll
-                for (int q = 0; q < kScoreChunkP; ++q) {
-                    if (q < np) {
-                        const double2 hv =
-                            __ldg(reinterpret_cast<const double2*>(h + (int64_t)(p0 + q) * n + j));
-                        acc[q] = fma(t.x, hv.x, acc[q]);
-                        acc[q] = fma(t.y, hv.y, acc[q]);
-                        sab[q] += fabs(t.x * hv.x) + fabs(t.y * hv.y);
-                    }
-                }
-            }
+    const double* h0 = h + (int64_t)min(p0 + rr, P - 1) * n;
+    const double* h1 = h + (int64_t)min(p0 + 8 + rr, P - 1) * n;
+    // k slice of this warp, in groups of 8 (two k-steps per 16-byte load: the
+    // k order inside a group is permuted identically for theta and h)
+    const int ng = (n + 7) / 8;
+    const int g0 = (int)((long long)ng * warp / kScoreSlices), g1 = (int)((long long)ng * (warp + 1) / kScoreSlices);
+    double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0, nrm = 0.0;
+    const bool vec = (n & 1) == 0;
+#pragma unroll 4
+    for (int gi = g0; gi < g1; ++gi) {
+        const int k = gi * 8 + 2 * cc;
+        double2 t, a, b;
+        if (vec && k + 1 < n) {
+            t = __ldg(reinterpret_cast<const double2*>(th + k));
+            a = __ldg(reinterpret_cast<const double2*>(h0 + k));
+            b = __ldg(reinterpret_cast<const double2*>(h1 + k));
         } else {
-            for (int j = lane; j < n; j += 32) {
-                const double t = __ldg(th + j);
-#pragma unroll
-                for (int q = 0; q < kScoreChunkP; ++q) {
-                    if (q < np) {
-                        const double hv = __ldg(h + (int64_t)(p0 + q) * n + j);
-                        acc[q] = fma(t, hv, acc[q]);
-                        sab[q] += fabs(t * hv);
-                    }
-                }
-            }
+            t.x = k < n ? th[k] : 0.0;  t.y = k + 1 < n ? th[k + 1] : 0.0;
+            a.x = k < n ? h0[k] : 0.0;  a.y = k + 1 < n ? h0[k + 1] : 0.0;
+            b.x = k < n ? h1[k] : 0.0;  b.y = k + 1 < n ? h1[k + 1] : 0.0;
         }
-#pragma unroll
-        for (int q = 0; q < kScoreChunkP; ++q) {
-            acc[q] = warp_sum(acc[q]);
-            sab[q] = warp_sum(sab[q]);
+        nrm = fma(t.y, t.y, fma(t.x, t.x, nrm));
+        dmma(d00, d01, t.x, a.x);
+        dmma(d10, d11, t.x, b.x);
+        dmma(d00, d01, t.y, a.y);
+        dmma(d10, d11, t.y, b.y);
+    }
+    // row-norm partial: the four k lanes of a row
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    part[warp][lane][0] = d00;
+    part[warp][lane][1] = d01;
+    part[warp][lane][2] = d10;
+    part[warp][lane][3] = d11;
+    part[warp][lane][4] = nrm;
+    __syncthreads();
+    if (threadIdx.x < 128) {  // (row i, prompt q) = (t / 16, t % 16)
+        const int i = threadIdx.x >> 4, q = threadIdx.x & 15;
+        // D fragment: lane L holds D[L >> 2][2 (L & 3) + {0, 1}] of tile q / 8
+        const int L = i * 4 + ((q & 7) >> 1), e = (q >= 8 ? 2 : 0) + (q & 1);
+        double acc = 0.0, nr = 0.0;
+        for (int w = 0; w < kScoreSlices; ++w) {
+            acc += part[w][L][e];
+            nr += part[w][i * 4][4];
         }
-        if (lane == 0) {
-            const double b = bias[row];
-            for (int q = 0; q < np; ++q) {
-                z[(int64_t)(p0 + q) * r + row] = acc[q] + b;
-                if (bnd) bnd[(int64_t)(p0 + q) * r + row] = gam * (sab[q] + fabs(b)) * 1.0000001 + tiny;
-            }
+        const int R = row0 + i, p = p0 + q;
+        if (R < r && p < P) {
+            const double gam = 4.0 * (double)(n + 2) * kU;
+            const double tiny = 4.0 * (double)(n + 2) * 4.9406564584124654e-324;
+            const double b = bias[R];
+            z[(int64_t)p * r + R] = acc + b;
+            if (bnd) bnd[(int64_t)p * r + R] = gam * (sqrt(nr) * hnorm[p] + fabs(b)) * 1.0000001 + tiny;
         }
     }
 }
@@ -286,7 +380,10 @@ k_route_select(const double* __restrict__ zfast, const double* __restrict__ bnd,
 template <typename TX>
 static void launch_mean_pool_t(const void* x, pg_layout lay, int n, int64_t ttot,
                                const int64_t* offs_dev, int P, double* h, cudaStream_t st) {
-    if (lay == PG_TOKEN_MAJOR) {
+    if (lay == PG_TOKEN_MAJOR && sizeof(TX) == 2 && n % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0) {
+        dim3 g((n / 2 + 127) / 128, P);
+        k_mean_pool_tm_bf16x2<<<g, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(x), n, offs_dev, h);
+    } else if (lay == PG_TOKEN_MAJOR) {
         dim3 g((n + 255) / 256, P);
         k_mean_pool_tm<TX><<<g, 256, 0, st>>>(static_cast<const TX*>(x), n, offs_dev, h);
     } else {
@@ -306,13 +403,16 @@ void launch_mean_pool(const void* x, pg_dtype dt, pg_layout lay, int n, int64_t 
 }
 
 void launch_score(const double* theta, const double* bias, int r, int n, const double* h, int P,
-                  double* z, double* bnd, int exact, cudaStream_t st) {
+                  double* z, double* bnd, int exact, cudaStream_t st, double* hnorm) {
     if (exact) {
         dim3 g((r + 127) / 128, P);
         k_score_exact<<<g, 128, 0, st>>>(theta, bias, r, n, h, P, z);
     } else {
-        k_score_fast<<<(r + kScoreWarps - 1) / kScoreWarps, kScoreWarps * 32, 0, st>>>(
-            theta, bias, r, n, h, P, z, bnd);
+        // hnorm: caller scratch of P doubles
+        k_hnorm<<<P, 256, 0, st>>>(h, n, hnorm);
+        PG_LAUNCH_CHECK();
+        dim3 g((r + 7) / 8, (P + 15) / 16);
+        k_score_fast<<<g, kScoreSlices * 32, 0, st>>>(theta, bias, r, n, h, hnorm, P, z, bnd);
     }
     PG_LAUNCH_CHECK();
 }

@@ -128,6 +128,40 @@ def test_route_select_multi_prompt(pg, port):
         assert np.array_equal(got[p].astype(np.uint32), want)
 
 
+def test_route_select_pooled_matches_reference(pg, port):
+    """Pool once, route several routers (q/k/v share hn): bit-exact per prompt;
+    20 prompts span two score passes; token counts around the pool batch."""
+    r, n, K = 530, 640, 211
+    lens = [1, 31, 32, 33, 70, 2, 5, 64, 9, 3, 40, 1, 7, 8, 16, 17, 63, 65, 4, 6]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    X = port.gaussian(91, (offs[-1], n))
+    Xd = torch.from_numpy(X).cuda()
+    h = pg.mean_pool(Xd, layout="token", offsets=offs)
+    for seed in (92, 93, 94):
+        theta = port.gaussian(seed, (r, n)); bias = port.gaussian(seed + 10, (r,))
+        router = pg.RouterParams(theta, bias)
+        got = pg.route_select_pooled(router, h, K).cpu().numpy()
+        direct = pg.route_select(router, Xd, K, layout="token", offsets=offs).cpu().numpy()
+        assert np.array_equal(got, direct)
+        for p in range(len(lens)):
+            want = port.select_topk(port.score(theta, bias, port.mean_pool(X[offs[p]:offs[p + 1]].T)), K)
+            assert np.array_equal(got[p].astype(np.uint32), want), (seed, p)
+
+
+def test_mean_pool_bf16_token_major_batched(pg, port):
+    """bf16 token-major pooling (two features per thread, 64 tokens in flight)
+    is the reference's sequential fp64 sum on the bf16 values, bit for bit."""
+    n = 1030
+    lens = [1, 63, 64, 65, 129, 200, 3]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    X = port.gaussian(95, (offs[-1], n))
+    Xb = torch.from_numpy(X).cuda().to(torch.bfloat16)
+    Xr = Xb.double().cpu().numpy()
+    h = pg.mean_pool(Xb, layout="token", offsets=offs).cpu().numpy()
+    for p in range(len(lens)):
+        assert np.array_equal(h[p], port.mean_pool(Xr[offs[p]:offs[p + 1]].T)), p
+
+
 def test_select_topk_ties_and_errors(pg):
     # test_router.cpp:75-83
     logits = [1.0, 2.0, 2.0, 1.0, 2.0]
