@@ -217,8 +217,8 @@ def gpu_arm(args, rank, world, local_rank):
 
     def step(i, host_io, fused=True):
         a = aggs[i % REPLICAS]
-        if host_io:
-            xs[i].copy_(x_host[i], non_blocking=True)
+        if host_io:  # per-token input H2D from pinned memory, as a PDL-chained kernel
+            pg.copy_io(xs[i], x_host[i])
         if fused:  # K6: whole MLP block in one kernel (up/gate fused B side, silu epilogue, down)
             pg.mlp_forward(a["up"], a["gate"], a["down"], 0, xs[i], out=y[i], act=act[i])
         else:      # aggregated-only: one chain kernel per linear + silu kernel
@@ -226,8 +226,8 @@ def gpu_arm(args, rank, world, local_rank):
             pg.aggregated_forward(a["gate"], 0, xs[i], out=gt[i])
             pg.silu_mul(gt[i], up[i], out=act[i])
             pg.aggregated_forward(a["down"], 0, act[i], out=y[i])
-        if host_io:
-            y_host[i].copy_(y[i], non_blocking=True)
+        if host_io:  # result D2H into pinned memory
+            pg.copy_io(y_host[i], y[i])
 
     stream = torch.cuda.Stream(device=dev)
     graphs = {}

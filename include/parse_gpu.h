@@ -256,6 +256,12 @@ void pg_make_patterns(uint64_t seed, size_t n_patterns, const size_t* r_stores,
 int pg_fill_normal_device(void* out_dev, pg_dtype dtype, size_t count, uint64_t seed,
                           double scale, pg_stream stream);
 
+/* Step I/O as a kernel: copy `bytes` between device-accessible buffers
+ * (device memory, or pinned host memory at its UVA address) on `stream`,
+ * chained to the neighbouring kernels by programmatic dependent launch -- the
+ * per-token H2D of x and D2H of y without copy-engine nodes in the step. */
+int pg_copy_io(const void* src, void* dst, size_t bytes, pg_stream stream);
+
 /* Diagnostics: with PG_CHAIN_DBG=1 the decode-chain kernel records per-CTA
  * %globaltimer stamps [cta][16] of its phases; copies the last launch's. */
 int pg_chain_debug_dump(uint64_t* out_host, size_t n);

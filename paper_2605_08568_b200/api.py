@@ -804,6 +804,22 @@ def mlp_forward(up: "AggregatedLayer", gate: "AggregatedLayer", down: "Aggregate
     return y
 
 
+def copy_io(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    """Step I/O as a kernel on the current stream: dst <- src where either side
+    may be pinned host memory (UVA-mapped).  Chains with the step's kernels
+    (programmatic dependent launch) instead of a copy-engine node."""
+    for t in (dst, src):
+        if not (t.is_cuda or t.is_pinned()):
+            raise ValueError("copy_io: buffers must be device or pinned host memory")
+        if not t.is_contiguous():
+            raise ValueError("copy_io: buffers must be contiguous")
+    nb = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() != nb:
+        raise ValueError("copy_io: size mismatch")
+    call("pg_copy_io", C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), nb, _stream())
+    return dst
+
+
 def silu_mul(gate: torch.Tensor, up: torch.Tensor, out_dtype=torch.bfloat16, out=None) -> torch.Tensor:
     """MLP glue (toy_lm.hpp:250-257): silu(gate) * up on device."""
     if gate.shape != up.shape or gate.dtype != up.dtype:

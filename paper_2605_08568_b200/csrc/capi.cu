@@ -23,6 +23,7 @@ void set_error(int code, const std::string& msg) {
 // ---- kernel launchers (route.cu, cache.cu, values.cu, umma.cu) ----
 void launch_mean_pool(const void* x, pg_dtype dt, pg_layout lay, int n, int64_t ttot,
                       const int64_t* offs_dev, int P, double* h, cudaStream_t st);
+void launch_copy_io(const void* src, void* dst, size_t bytes, cudaStream_t st);
 void launch_score(const double* theta, const double* bias, int r, int n, const double* h, int P,
                   double* z, double* bnd, int exact, cudaStream_t st, double* hnorm = nullptr);
 void launch_select_topk(const double* logits, int r, int P, int K, uint32_t* sel, cudaStream_t st);
@@ -1104,6 +1105,13 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, 
         const LinSpec& D = ph[1][0];
         run_forward(up->dt, D.bt, D.ldb, D.a, D.lda, D.sm, D.cap, D.n, D.m, a, 0, 1, y, ydt, st);
     }
+    PG_API_END
+}
+
+int pg_copy_io(const void* src, void* dst, size_t bytes, pg_stream s) {
+    PG_API_BEGIN
+    require(src && dst, PG_INVALID_ARGUMENT, "copy_io: null buffer");
+    launch_copy_io(src, dst, bytes, as_stream(s));
     PG_API_END
 }
 

@@ -95,6 +95,42 @@ void launch_fill_normal(void* out, pg_dtype dt, size_t count, uint64_t seed, dou
     else k_fill_normal<__nv_bfloat16><<<blocks, 256, 0, st>>>(static_cast<__nv_bfloat16*>(out), count, seed, scale);
     PG_LAUNCH_CHECK();
 }
+// Step I/O as a kernel: copies between device-accessible buffers (device
+// memory or pinned host memory, which UVA maps at the same address), so a
+// decode step's input / output transfers chain with the step's kernels under
+// programmatic dependent launch instead of splitting the stream with copy-engine
+// nodes.  16-byte vectors when both ends allow it.
+__global__ void __launch_bounds__(256) k_copy_io(const unsigned char* __restrict__ src,
+                                                 unsigned char* __restrict__ dst, size_t bytes) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the predecessor may produce src
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const size_t n16 = bytes / 16;
+        for (size_t i = tid; i < n16; i += nt)
+            reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+        for (size_t i = n16 * 16 + tid; i < bytes; i += nt) dst[i] = src[i];
+    } else {
+        for (size_t i = tid; i < bytes; i += nt) dst[i] = src[i];
+    }
+}
+
+void launch_copy_io(const void* src, void* dst, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    const int blocks = (int)std::min<size_t>(64, (bytes / 16 + 255) / 256 + 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_copy_io, static_cast<const unsigned char*>(src),
+                                     static_cast<unsigned char*>(dst), bytes));
+    count_launch();
+}
 }  // namespace pg
 
 extern "C" {

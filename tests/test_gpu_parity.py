@@ -162,6 +162,20 @@ def test_mean_pool_bf16_token_major_batched(pg, port):
         assert np.array_equal(h[p], port.mean_pool(Xr[offs[p]:offs[p + 1]].T)), p
 
 
+@pytest.mark.parametrize("nbytes", [1, 15, 16, 8192, 16384 + 7])
+def test_copy_io_pinned_roundtrip(pg, nbytes):
+    src = torch.randint(0, 255, (nbytes,), dtype=torch.uint8).pin_memory()
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    back = torch.zeros(nbytes, dtype=torch.uint8).pin_memory()
+    pg.copy_io(dev, src)
+    pg.copy_io(back, dev)
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)
+    assert torch.equal(dev.cpu(), src)
+    with pytest.raises(ValueError):
+        pg.copy_io(torch.empty(nbytes + 1, dtype=torch.uint8, device="cuda"), src)
+
+
 def test_select_topk_ties_and_errors(pg):
     # test_router.cpp:75-83
     logits = [1.0, 2.0, 2.0, 1.0, 2.0]
