@@ -176,6 +176,30 @@ def test_copy_io_pinned_roundtrip(pg, nbytes):
         pg.copy_io(torch.empty(nbytes + 1, dtype=torch.uint8, device="cuda"), src)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_expert_sharded_partials_sum_to_full(pg, port, world):
+    """Expert-sharded linear (e mod G): the per-rank partials through the GPU
+    kernels sum to the single-GPU result (reduction order only); world 1
+    exercises the collective-free path of ShardedLinear."""
+    from paper_2605_08568_b200 import dist as pgd
+    m, n, r, K, T = 320, 256, 192, 96, 5
+    A = port.gaussian(61, (m, r)); B = port.gaussian(62, (n, r))
+    x = port.gaussian(63, (n, T))
+    sel = pg.RankSelection(np.sort(np.random.default_rng(64).choice(r, K, replace=False)).astype(np.uint32))
+    xd = torch.from_numpy(x).cuda().float()
+    want = port.masked_forward(A, B, sel.indices, x.astype(np.float32).astype(np.float64))
+    total = 0
+    for rank in range(world):
+        if world == 1:
+            total = pgd.ShardedLinear(A, B, 1, 0, dtype="f32").forward(sel, xd).double().cpu().numpy()
+        else:
+            lin = pgd.ShardedLinear(A, B, world, rank, dtype="f32")
+            mine = pgd.shard_selection(sel, world, rank)
+            ids = lin.shard.local_ids(mine)
+            total = total + pg.masked_forward(lin.local, pg.RankSelection(ids), xd).double().cpu().numpy()
+    assert np.abs(total - want).max() / np.abs(want).max() <= 1e-5
+
+
 def test_select_topk_ties_and_errors(pg):
     # test_router.cpp:75-83
     logits = [1.0, 2.0, 2.0, 1.0, 2.0]
