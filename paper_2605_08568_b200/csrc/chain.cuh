@@ -5,7 +5,7 @@
 
 namespace pg {
 
-constexpr int kChainThreads = 512;
+constexpr int kChainThreads = 384;
 constexpr int kChainWarps = kChainThreads / 32;
 constexpr int kConsumerWarps = kChainWarps - 1;  // warp 15 is the TMA producer
 constexpr int kMaxLin = 3;

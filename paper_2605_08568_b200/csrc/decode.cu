@@ -188,6 +188,91 @@ __device__ __forceinline__ A zdot(const int4& wraw, const A* z, int pl, int v, A
     return acc;
 }
 
+
+// ---- bf16 fast paths: f32x2 FMAs (sm_100 FFMA2) on bf16 pairs, every load of
+// a row issued before the math, no per-vector branches (a vector past the row
+// re-reads vector 0 and is zeroed by a select).
+__device__ __forceinline__ void ffma2(float2& d, const float2& a, const float2& b) {
+    asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rd, {%0, %1};\n"
+        " fma.rn.f32x2 rd, ra, rb, rd;\n mov.b64 {%0, %1}, rd;\n}"
+        : "+f"(d.x), "+f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+}
+__device__ __forceinline__ float2 bf2(uint32_t h) {  // bf16 pair -> (lo, hi) f32
+    return make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u));
+}
+constexpr int kRowJ = 5;  // 16-byte vectors per lane per batch of a stage-2 row
+// stage 2: A_S row (bf16, nv vectors) . z (f32, two-plane smem layout)
+__device__ __forceinline__ float row_dot_bf16(const int4* r, int nv, const float* z, int pl, int lane) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+    for (int v0 = 0; v0 < nv; v0 += 32 * kRowJ) {
+        int4 w[kRowJ];
+        float4 zl[kRowJ], zh[kRowJ];
+#pragma unroll
+        for (int j = 0; j < kRowJ; ++j) {
+            const int v = v0 + 32 * j + lane;
+            const bool ok = v < nv;
+            const int vv = ok ? v : 0;
+            const int4 t = lds128(r + vv);
+            w[j] = ok ? t : make_int4(0, 0, 0, 0);
+            zl[j] = lds128f(z + vv * 4);
+            zh[j] = lds128f(z + pl + vv * 4);
+        }
+#pragma unroll
+        for (int j = 0; j < kRowJ; ++j) {
+            ffma2(a0, bf2((uint32_t)w[j].x), make_float2(zl[j].x, zl[j].y));
+            ffma2(a1, bf2((uint32_t)w[j].y), make_float2(zl[j].z, zl[j].w));
+            ffma2(a0, bf2((uint32_t)w[j].z), make_float2(zh[j].x, zh[j].y));
+            ffma2(a1, bf2((uint32_t)w[j].w), make_float2(zh[j].z, zh[j].w));
+        }
+    }
+    return (a0.x + a0.y) + (a1.x + a1.y);
+}
+// stage 2 with z in registers: zr[j] = the 8 z values of vector lane + 32 j
+// (zero past the row), loaded once per phase; only the weights come from smem.
+struct ZReg {
+    float2 p[kRowJ][4];
+};
+__device__ __forceinline__ void zreg_load(ZReg& zr, const float* z, int pl, int nv, int lane) {
+#pragma unroll
+    for (int j = 0; j < kRowJ; ++j) {
+        const int v = 32 * j + lane;
+        const bool ok = v < nv;
+        const float4 lo = lds128f(z + (ok ? v : 0) * 4), hi = lds128f(z + pl + (ok ? v : 0) * 4);
+        zr.p[j][0] = ok ? make_float2(lo.x, lo.y) : make_float2(0.f, 0.f);
+        zr.p[j][1] = ok ? make_float2(lo.z, lo.w) : make_float2(0.f, 0.f);
+        zr.p[j][2] = ok ? make_float2(hi.x, hi.y) : make_float2(0.f, 0.f);
+        zr.p[j][3] = ok ? make_float2(hi.z, hi.w) : make_float2(0.f, 0.f);
+    }
+}
+__device__ __forceinline__ float row_dot_zreg(const int4* r, int nv, const ZReg& zr, int lane) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+    int4 w[kRowJ];
+#pragma unroll
+    for (int j = 0; j < kRowJ; ++j) w[j] = lds128(r + min(32 * j + lane, nv - 1));  // z is 0 past the row
+#pragma unroll
+    for (int j = 0; j < kRowJ; ++j) {
+        ffma2(a0, bf2((uint32_t)w[j].x), zr.p[j][0]);
+        ffma2(a1, bf2((uint32_t)w[j].y), zr.p[j][1]);
+        ffma2(a0, bf2((uint32_t)w[j].z), zr.p[j][2]);
+        ffma2(a1, bf2((uint32_t)w[j].w), zr.p[j][3]);
+    }
+    return (a0.x + a0.y) + (a1.x + a1.y);
+}
+// stage 1: B^T row (bf16, nv vectors) . x (bf16 smem)
+__device__ __forceinline__ float row_dot_x_bf16(const int4* r, const int4* x, int nv, int lane) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+#pragma unroll 4
+    for (int v = lane; v < nv; v += 32) {
+        const int4 w = lds128(r + v), xx = lds128(x + v);
+        ffma2(a0, bf2((uint32_t)w.x), bf2((uint32_t)xx.x));
+        ffma2(a1, bf2((uint32_t)w.y), bf2((uint32_t)xx.y));
+        ffma2(a0, bf2((uint32_t)w.z), bf2((uint32_t)xx.z));
+        ffma2(a1, bf2((uint32_t)w.w), bf2((uint32_t)xx.w));
+    }
+    return (a0.x + a0.y) + (a1.x + a1.y);
+}
+
 __device__ __forceinline__ bool slot_on(const LinS& L, int s) {
     return s >= L.run0 || L.mask == nullptr || L.mask[s] != 0;
 }
@@ -416,13 +501,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                     const int4* rv = reinterpret_cast<const int4*>(base + (size_t)q * rb);
                     const int4* xv = reinterpret_cast<const int4*>(xs);
                     A acc = A(0);
+                    if constexpr (sizeof(W) == 2) {
+                        acc = row_dot_x_bf16(rv, xv, nv, lane);
+                    } else {
 #pragma unroll 4
-                    for (int v = lane; v < nv; v += 32) {
-                        A wv[V], xx[V];
-                        cunpack<W, A>(lds128(rv + v), wv);
-                        cunpack<W, A>(lds128(xv + v), xx);
+                        for (int v = lane; v < nv; v += 32) {
+                            A wv[V], xx[V];
+                            cunpack<W, A>(lds128(rv + v), wv);
+                            cunpack<W, A>(lds128(xv + v), xx);
 #pragma unroll
-                        for (int t = 0; t < V; ++t) acc = fma(wv[t], xx[t], acc);
+                            for (int t = 0; t < V; ++t) acc = fma(wv[t], xx[t], acc);
+                        }
                     }
                     acc = warp_sum(acc);
                     if (lane == 0) {
@@ -474,6 +563,21 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         }
         consumer_sync();
         STAMP(ph * 6 + 4);
+        // bf16 with <= 2 linears of <= 32 * 8 * kRowJ slots: z into registers
+        ZReg zr0, zr1;
+        bool zreg = false;
+        if constexpr (sizeof(W) == 2) {
+            zreg = nlin <= 2;
+            for (int l = 0; l < nlin; ++l) zreg = zreg && L[l].nslots <= 32 * V * kRowJ;
+            if (zreg) {
+                const int ns0 = L[0].nslots;
+                zreg_load(zr0, zs + zoff[0], (ns0 + 7) / 8 * 4, ns0 / V, lane);
+                if (nlin > 1) {
+                    const int ns1 = L[1].nslots;
+                    zreg_load(zr1, zs + zoff[1], (ns1 + 7) / 8 * 4, ns1 / V, lane);
+                }
+            }
+        }
         // ---- stage 2: y_i = A_S[i] . z
         for (;;) {
             mbar_wait(smem_u32(&full[k]), (par >> k) & 1u);
@@ -493,11 +597,21 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                         const A* z1 = zs + zoff[1];
                         const int pl0 = (ns0 + 7) / 8 * 4, pl1 = (ns1 + 7) / 8 * 4;
                         A a0 = A(0), a1 = A(0);
-                        for (int v = lane; v < ns0 / V; v += 32) {
-                            a0 = zdot<W, A>(lds128(r0 + v), z0, pl0, v, a0);
-                        }
-                        for (int v = lane; v < ns1 / V; v += 32) {
-                            a1 = zdot<W, A>(lds128(r1 + v), z1, pl1, v, a1);
+                        if constexpr (sizeof(W) == 2) {
+                            if (zreg) {
+                                a0 = row_dot_zreg(r0, ns0 / V, zr0, lane);
+                                a1 = row_dot_zreg(r1, ns1 / V, zr1, lane);
+                            } else {
+                                a0 = row_dot_bf16(r0, ns0 / V, z0, pl0, lane);
+                                a1 = row_dot_bf16(r1, ns1 / V, z1, pl1, lane);
+                            }
+                        } else {
+                            for (int v = lane; v < ns0 / V; v += 32) {
+                                a0 = zdot<W, A>(lds128(r0 + v), z0, pl0, v, a0);
+                            }
+                            for (int v = lane; v < ns1 / V; v += 32) {
+                                a1 = zdot<W, A>(lds128(r1 + v), z1, pl1, v, a1);
+                            }
                         }
                         a0 = warp_sum(a0);
                         a1 = warp_sum(a1);
@@ -516,8 +630,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                         const A* z = zs + zoff[l];
                         const int pl = (ns + 7) / 8 * 4;
                         A acc = A(0);
-                        for (int v = lane; v < ns / V; v += 32) {
-                            acc = zdot<W, A>(lds128(r + v), z, pl, v, acc);
+                        if constexpr (sizeof(W) == 2) {
+                            if (zreg) acc = l == 0 ? row_dot_zreg(r, ns / V, zr0, lane) : row_dot_zreg(r, ns / V, zr1, lane);
+                            else acc = row_dot_bf16(r, ns / V, z, pl, lane);
+                        } else {
+                            for (int v = lane; v < ns / V; v += 32) {
+                                acc = zdot<W, A>(lds128(r + v), z, pl, v, acc);
+                            }
                         }
                         acc = warp_sum(acc);
                         if (lane == 0) {
