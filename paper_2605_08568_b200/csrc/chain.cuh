@@ -21,7 +21,7 @@ struct ChainLin {
     SlotMap sm;      // runs + activity mask (no gather lists), resolved on device
     int cap;         // slots upper bound
     int n, m;
-    void* zpart;     // [cap] accumulator-precision z (global exchange between CTAs)
+    void* zpart;     // [cap * (f64 ? 2 : 1)] tagged z words (cross-CTA exchange)
     void* y;         // output (epilogue 0)
 };
 
@@ -37,7 +37,9 @@ struct ChainPhase {
 struct ChainParams {
     int nphase;
     ChainPhase ph[kMaxPhase];
-    unsigned long long* bar;  // grid-barrier counter (zeroed per launch)
+    unsigned long long* bar;    // grid-barrier counter (act hand-over between MLP phases)
+    unsigned long long* epoch;  // launch counter (each CTA adds 1 per launch): z-word tags
+    int ztag;                   // 1: z exchanged as tagged words (MLP); 0: plain z + grid barrier
     int xs_bytes;             // shared-memory x region (max over phases)
     int zs_bytes;             // shared-memory z region (max over phases)
     int chunk_bytes;          // ring stage size

@@ -136,6 +136,30 @@ __device__ __forceinline__ void grid_sync_consumers(unsigned long long* bar) {
     consumer_sync();
 }
 
+// ---- z exchange: tagged 64-bit words {payload (low 32), launch tag (high 32)},
+// one relaxed gpu-scope store each, polled by the readers until the tag
+// matches.  No fence -- a release would compile to MEMBAR.GPU, which waits
+// for the SM's in-flight bulk copies (the whole ring).
+__device__ __forceinline__ void xput(unsigned long long* p, uint32_t payload, uint32_t tag) {
+    const unsigned long long v = ((unsigned long long)tag << 32) | payload;
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long xget(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+template <typename A>
+__device__ __forceinline__ void xput_acc(unsigned long long* zx, int s, A v, uint32_t tag) {
+    if constexpr (sizeof(A) == 4) {
+        xput(zx + s, __float_as_uint(v), tag);
+    } else {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+        xput(zx + 2 * s, (uint32_t)b, tag);
+        xput(zx + 2 * s + 1, (uint32_t)(b >> 32), tag);
+    }
+}
+
 // Copy `count` elements global -> shared with every thread's loads issued
 // before any store (one latency instead of one per loop trip).
 template <typename T, int B>
@@ -415,7 +439,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     Desc* descs = reinterpret_cast<Desc*>(smem + 1024 + P.xs_bytes + P.zs_bytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(descs + kRingStages);
     uint64_t* empty = full + kRingStages;
-    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char*>(empty + kRingStages) - smem) + 127) & ~size_t(127);
+    const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char*>(empty + kRingStages) - smem) + 16 + 127) & ~size_t(127);
     unsigned char* ring = smem + ring_off;
     const int nst = (int)min((size_t)min(P.max_stages, kRingStages), (size_t)(227 * 1024 - ring_off) / (size_t)P.chunk_bytes);
 
@@ -463,6 +487,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         if (lane == 0) chain_producer<W>(P, lins, descs, full, empty, ring, nst);
         return;
     }
+    // launch tag: every CTA adds 1 to the workspace's epoch counter before it
+    // publishes anything, and a CTA of the next launch becomes resident only
+    // after a CTA of this one exited, so old / G is the launch index.
+    unsigned long long epoch_old = 0;
+    if (threadIdx.x == 0) epoch_old = atomicAdd(P.epoch, 1ull);
+    uint32_t* tag_s = reinterpret_cast<uint32_t*>(empty + kRingStages);
     // consumers read x and write z / act / y: wait for the previous grid
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
@@ -483,7 +513,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             for (int e = (nbytes / 16) * 16 / es + tid; e < n; e += nct) xs[e] = static_cast<const W*>(Q.x)[e];
             for (int e = n + tid; e < (n + V - 1) / V * V; e += nct) xs[e] = W(0);
         }
+        if (ph == 0 && threadIdx.x == 0) *tag_s = (uint32_t)(epoch_old / (unsigned long long)G) + 1u;
         consumer_sync();
+        const uint32_t tag = *tag_s;
         STAMP(ph * 6 + 1);
         // ---- stage 1: z_s = B^T[s] . x
         for (;;) {
@@ -516,7 +548,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                     acc = warp_sum(acc);
                     if (lane == 0) {
                         const int s = D.ids[q];  // masked slots publish 0 (exec_engine.hpp:221-223)
-                        static_cast<A*>(Ls.z)[s] = slot_on(Ls, s) ? acc : A(0);
+                        const A zv = slot_on(Ls, s) ? acc : A(0);
+                        if (P.ztag) xput_acc<A>(static_cast<unsigned long long*>(Ls.z), s, zv, tag);
+                        else static_cast<A*>(Ls.z)[s] = zv;
                     }
                 }
             }
@@ -526,7 +560,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             if (last) break;
         }
         STAMP(ph * 6 + 2);
-        grid_sync_consumers(P.bar);
+        if (!P.ztag) grid_sync_consumers(P.bar);
         STAMP(ph * 6 + 3);
         // ---- z into shared memory (inactive slots -> 0)
         int zoff[kMaxLin];
@@ -534,27 +568,44 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             int o = 0;
             for (int l = 0; l < nlin; ++l) {
                 zoff[l] = o;
-                const A* z = static_cast<const A*>(L[l].z);
+                const unsigned long long* zx = static_cast<const unsigned long long*>(L[l].z);
                 const int ns = L[l].nslots;
-                // inactive slots were already written as 0 by stage 1; loads are
-                // batched so each thread pays one L2 round trip, not one per slot
+                // every thread's polls of a batch are issued before any is
+                // checked (one L2 round trip per batch, not one per slot)
                 constexpr int B = 8;
+                constexpr int zw = sizeof(A) / 4;
                 const int pl = (ns + 7) / 8 * 4;
                 for (int base = 0; base < ns; base += B * nct) {
-                    A v[B];
+                    unsigned long long v[B][zw];
 #pragma unroll
                     for (int u = 0; u < B; ++u) {
                         const int s = base + u * nct + tid;
-                        if (s < ns) v[u] = z[s];
+                        if (P.ztag) {
+#pragma unroll
+                            for (int h = 0; h < zw; ++h) v[u][h] = s < ns ? xget(zx + (size_t)s * zw + h) : 0ull;
+                        }
                     }
 #pragma unroll
                     for (int u = 0; u < B; ++u) {
                         const int s = base + u * nct + tid;
                         if (s < ns) {
+                            A val;
+                            if (P.ztag) {
+                                unsigned long long w[zw];
+#pragma unroll
+                                for (int h = 0; h < zw; ++h) {
+                                    w[h] = v[u][h];
+                                    while ((uint32_t)(w[h] >> 32) != tag) w[h] = xget(zx + (size_t)s * zw + h);
+                                }
+                                if constexpr (zw == 1) val = __uint_as_float((uint32_t)w[0]);
+                                else val = __longlong_as_double((long long)((w[1] << 32) | (w[0] & 0xffffffffull)));
+                            } else {
+                                val = reinterpret_cast<const A*>(zx)[s];  // published before the barrier
+                            }
                             // bf16: two planes (slots 0-3 / 4-7 of every 8) so each
                             // lane's 8 z-values are two conflict-free 16-byte loads
-                            if constexpr (V == 8) zs[o + (s >> 3) * 4 + (s & 3) + ((s & 4) ? pl : 0)] = v[u];
-                            else zs[o + s] = v[u];
+                            if constexpr (V == 8) zs[o + (s >> 3) * 4 + (s & 3) + ((s & 4) ? pl : 0)] = val;
+                            else zs[o + s] = val;
                         }
                     }
                 }
