@@ -1,3 +1,4 @@
 O=gpurun_out; mkdir -p $O
-for i in 1 2; do for z in 0 1; do echo "ztag $z"; PG_CHAIN_ZTAG=$z timeout 120 python tools/exp_decode.py 4 2048; done; done > $O/ec2.txt 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "chain or mlp or module or aggregated or decode or masked" 2>&1 | tail -2 > $O/ec2.txt
+for a in 0 4 8 16; do echo "l2ahead $a"; PG_CHAIN_L2AHEAD=$a timeout 120 python tools/exp_decode.py 4 2048; done >> $O/ec2.txt 2>&1
 cat $O/ec2.txt
