@@ -78,6 +78,18 @@ int main(int argc, char** argv) {
         fm.routers[id] = r;
     }
     save_factorized(out / "factorized", fm);
+    // the reference's prompt embedding (block-0 output of the static-prefix
+    // model, mean-pooled and normalised; pattern_cache.hpp:50-65, :84)
+    {
+        const std::vector<std::uint8_t> toks = {1, 5, 2, 7, 3, 0, 6};
+        FactorizedProvider emb_prov(fm);
+        const PromptEmbedding pe = embed_prompt(fm.core, emb_prov, toks, "golden");
+        std::ofstream ef(out / "embed.f64", std::ios::binary);
+        ef.write(reinterpret_cast<const char*>(pe.vec.data()), std::streamsize(pe.vec.size() * 8));
+        std::ofstream tf(out / "embed_tokens.txt");
+        for (auto t : toks) tf << int(t) << " ";
+        tf << "\n";
+    }
     // pattern cache: 6 entries, unit-norm embeddings, per-tensor selections
     PatternCache cache;
     cache.d_model = d;

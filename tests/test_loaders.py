@@ -80,3 +80,23 @@ def test_load_cache_retrieves_like_the_reference():
     assert res.entry == int(entry) and res.hit == bool(int(hit))
     assert res.similarity == float(sim)
     assert res.pattern is cache.entries[int(entry)].pattern
+
+
+@pytest.mark.gpu
+def test_embed_prompt_on_device_matches_reference():
+    """embed_prompt (pattern_cache.hpp:50-65): block-0 forward of the static-
+    prefix model on device, pooled and normalised, vs the reference's own."""
+    import paper_2605_08568_b200 as pg
+    from paper_2605_08568_b200 import embed, loaders
+    model = loaders.load_factorized(os.path.join(GOLD, "factorized"), dtype="f64")
+    toks = [int(t) for t in open(os.path.join(GOLD, "embed_tokens.txt")).read().split()]
+    want = np.fromfile(os.path.join(GOLD, "embed.f64"))
+    got = embed.embed_prompt(model, toks, source="golden")
+    assert got.source == "golden"
+    assert np.abs(np.asarray(got.vec) - want).max() <= 1e-12
+    cache = loaders.load_cache(os.path.join(GOLD, "cache"))
+    a = pg.retrieve(cache, got.vec)
+    b = pg.retrieve(cache, want)
+    assert (a.entry, a.hit) == (b.entry, b.hit)
+    with pytest.raises(ValueError):
+        embed.embed_prompt(model, [])
