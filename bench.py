@@ -348,14 +348,22 @@ def prefill_arm(pg, torch, dev, world, P=16, T=2048):
     src = {"q": X, "k": X, "v": X, "up": X, "gate": X, "o": Xo, "down": X2}
     sels = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for rep in range(2):
-        e0.record()
+
+    def route_all():
         pooled = {id(x): pg.mean_pool(x, layout="token", offsets=offs) for x in (X, Xo, X2)}
         for nm in lin:
             sels[nm] = pg.route_select_pooled(routers[nm], pooled[id(src[nm])], layers[nm][1])
-        e1.record()
-        torch.cuda.synchronize()
-    route_ms = e0.elapsed_time(e1)
+
+    for _ in range(3):  # warm: scratch pools, kernel attributes
+        route_all()
+    torch.cuda.synchronize()
+    route_reps = 5
+    e0.record()
+    for _ in range(route_reps):
+        route_all()
+    e1.record()
+    torch.cuda.synchronize()
+    route_ms = e0.elapsed_time(e1) / route_reps
     # pack each prompt's experts once (serving: after routing / a cache hit)
     t0 = time.perf_counter()
     aggs = {nm: [pg.aggregate_layout(layers[nm][0], [pg.RankSelection(sels[nm][p].cpu().numpy())], PSI)
