@@ -590,3 +590,48 @@ def test_module_forward_qkv_gqa(pg, port):
             A, B = data[i]
             ref = port.masked_forward(A.astype(np.float32), B.astype(np.float32), pats[pid][i], x)
             assert rel(y.cpu().numpy()[:, None], ref) <= TOL32
+
+
+def test_config2_mlp_decode_full_size(pg, port):
+    """BASELINE config 2 at full size: LLaMA-7B MLP block (11008 x 4096, ratio
+    0.6, K=1194, r_store=2388), bf16, one pattern-cache selection reused over
+    decode steps -- the bench's kernel -- vs the oracle composition."""
+    d, ff = 4096, 11008
+    K = pg.single_layer_k(ff, d, 0.6); r = pg.store_rank(K, d)
+    assert (K, r) == (1194, 2388)
+    from oracle import pyoracle
+    pats = pyoracle.make_patterns(17171, 1, [(r, K)] * 3)[0]
+    data = {nm: make_layer_data(port, *(shp + (r, 70 + i))) for i, (nm, shp) in
+            enumerate([("up", (ff, d)), ("gate", (ff, d)), ("down", (d, ff))])}
+    aggs = {nm: pg.aggregate_layout(pg.FactorizedLayer(*data[nm], K, dtype="bf16"), [pg.RankSelection(pats[i])], 0.9)
+            for i, nm in enumerate(("up", "gate", "down"))}
+    rd = {nm: (bf16_round(A), bf16_round(B)) for nm, (A, B) in data.items()}
+    for step in range(3):  # the frozen selection serves every decode step
+        x = port.gaussian(80 + step, (d, 1))
+        y = pg.mlp_forward(aggs["up"], aggs["gate"], aggs["down"], 0, torch.from_numpy(x).cuda().to(torch.bfloat16))
+        xr = bf16_round(x)
+        u = port.masked_forward(*rd["up"], pats[0], xr)
+        g = port.masked_forward(*rd["gate"], pats[1], xr)
+        ref = port.masked_forward(*rd["down"], pats[2], bf16_round(_silu(g) * u))
+        assert rel(y.double().cpu().numpy()[:, None], ref) <= 2e-3
+
+
+def test_config5_13b_shapes_decode_and_prefill(pg, port):
+    """BASELINE config 5 shapes: LLaMA-13B up-projection (13824 x 5120) at ratio
+    0.4 (K=2241, r_store=4482) -- wider than the single-launch chain's shared
+    memory, so decode takes the multi-kernel path -- T=1 and a T=64 prefill."""
+    m, n = 13824, 5120
+    K = pg.single_layer_k(m, n, 0.4); r = pg.store_rank(K, n)
+    assert (K, r) == (2241, 4482)
+    A, B = make_layer_data(port, m, n, r, 90)
+    Ar, Br = bf16_round(A), bf16_round(B)
+    sel = np.sort(np.random.default_rng(91).choice(r, K, replace=False)).astype(np.uint32)
+    L = pg.FactorizedLayer(A, B, K, dtype="bf16")
+    agg = pg.aggregate_layout(L, [pg.RankSelection(sel)], 0.9)
+    x1 = port.gaussian(92, (n, 1))
+    y1 = pg.aggregated_forward(agg, 0, torch.from_numpy(x1).cuda().to(torch.bfloat16))
+    assert rel(y1.double().cpu().numpy().reshape(-1, 1), port.masked_forward(Ar, Br, sel, bf16_round(x1))) <= 1e-4
+    x = port.gaussian(93, (n, 64))
+    y = pg.masked_forward(L, pg.RankSelection(sel), torch.from_numpy(x).cuda().to(torch.bfloat16))
+    # prefill rounds z to bf16 between the two tcgen05 stages
+    assert rel(y.double().cpu().numpy(), port.masked_forward(Ar, Br, sel, bf16_round(x))) <= 1e-2
