@@ -16,6 +16,8 @@
 // Roofline: tensor-pipe-bound, 2*M*N*K flops per group.
 #include <cuda.h>
 
+#include <cstdio>
+
 #include <algorithm>
 #include <memory>
 #include <mutex>
@@ -250,6 +252,221 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+
+// ---------------------------------------------------------------- 2-CTA variant
+// CTA pair (cluster of 2, cta_group::2): 256 x BN tiles, each CTA of the pair
+// loads its 128 rows of A and its BN/2 rows of B; the leader's single thread
+// issues tcgen05.mma.cta_group::2 (M = 256) over both CTAs' shared memory and
+// each CTA's TMEM receives its 128 rows.  Half the shared-memory bytes per
+// MMA of the 1-CTA kernel, so the ring is 6 stages deep.
+constexpr int U2_STAGES = 6;
+constexpr int U2_A_BYTES = UM_BM * UM_BK * 2;                 // 16 KB (this CTA's 128 rows)
+constexpr int U2_B_BYTES = (UM_BN_MAX / 2) * UM_BK * 2;       // 16 KB (this CTA's BN/2 rows)
+constexpr int U2_STAGE_BYTES = U2_A_BYTES + U2_B_BYTES;
+constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the leader CTA's copy of a barrier (shared::cluster address with the peer bit cleared)
+__device__ __forceinline__ uint32_t leader_addr(uint32_t local) { return local & 0xFEFFFFFFu; }
+__device__ __forceinline__ void u_mbar_arrive_tx_cluster(uint32_t b, uint32_t bytes) {
+    // relaxed: registering the expected bytes orders nothing (a release would
+    // be a fence that waits for this SM's in-flight TMA loads)
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void u_mbar_arrive_cluster(uint32_t b) {
+    // relaxed: the TMEM reads are ordered by tcgen05.fence::before_thread_sync
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void u_tma_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void u_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void u_commit2(uint32_t bar) {  // arrive on this barrier in both CTAs of the pair
+    asm volatile(
+        "{\n .reg .b16 m;\n mov.b16 m, 3;\n"
+        " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}"
+        ::"r"(bar)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_constant__ UmmaParams P) {
+    extern __shared__ __align__(1024) unsigned char usmem[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(usmem) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + U2_STAGES * U2_STAGE_BYTES);
+    uint64_t* full = bars;                        // [STAGES] (used in the leader)
+    uint64_t* empty = bars + U2_STAGES;           // [STAGES] (each CTA)
+    uint64_t* tfull = bars + 2 * U2_STAGES;       // [2] (each CTA)
+    uint64_t* tempty = bars + 2 * U2_STAGES + 2;  // [2] (used in the leader: both CTAs' epilogues)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * U2_STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < U2_STAGES; ++s) {
+            u_mbar_init(u_smem(&full[s]), 1);
+            u_mbar_init(u_smem(&empty[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            u_mbar_init(u_smem(&tfull[a]), 1);
+            u_mbar_init(u_smem(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // same warp in both CTAs: 2 accumulators x 256 columns
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(u_smem(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (both CTAs)
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = pair; t < P.total_tiles; t += npairs) {
+                int g = 0;
+                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+                const UmmaGroup& G = P.groups[g];
+                const int lt = t - G.tile_base;
+                const int m0 = (lt % G.tiles_m) * 2 * UM_BM + (int)rank * UM_BM;
+                const int n0 = (lt / G.tiles_m) * G.bn + (int)rank * (G.bn / 2);
+                const int kbs = (G.K + UM_BK - 1) / UM_BK;
+                const uint32_t bytes = 2 * (UM_A_BYTES + (uint32_t)(G.bn / 2) * UM_BK * 2);  // both CTAs
+                for (int kb = 0; kb < kbs; ++kb) {
+                    u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
+                    const uint32_t fb = leader_addr(u_smem(&full[s]));
+                    if (leader) u_mbar_arrive_tx_cluster(fb, bytes);
+                    unsigned char* st = base + s * U2_STAGE_BYTES;
+                    u_tma_2d_pair(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
+                    u_tma_2d_pair(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
+                    if (++s == U2_STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (leader && lane == 0) {
+            int s = 0, acc = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int t = pair; t < P.total_tiles; t += npairs) {
+                int g = 0;
+                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+                const UmmaGroup& G = P.groups[g];
+                const int kbs = (G.K + UM_BK - 1) / UM_BK;
+                const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(G.bn >> 3) << 17) |
+                                       ((uint32_t)((2 * UM_BM) >> 4) << 24);
+                u_mbar_wait(u_smem(&tempty[acc]), aph ^ 1);  // both CTAs drained this accumulator
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(acc * UM_BN_MAX);
+                for (int kb = 0; kb < kbs; ++kb) {
+                    u_mbar_wait(u_smem(&full[s]), ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = u_smem(base + s * U2_STAGE_BYTES), sb = sa + U2_A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < UM_BK / 16; ++k)
+                        u_mma2(d, u_desc(sa + k * 32), u_desc(sb + k * 32), idesc, (kb | k) != 0);
+                    u_commit2(u_smem(&empty[s]));  // frees the stage in both CTAs
+                    if (++s == U2_STAGES) { s = 0; ph ^= 1; }
+                }
+                u_commit2(u_smem(&tfull[acc]));  // accumulator ready in both CTAs
+                if (++acc == 2) { acc = 0; aph ^= 1; }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2-5, both CTAs)
+        const int q = warp & 3;
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = pair; t < P.total_tiles; t += npairs) {
+            int g = 0;
+            while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+            const UmmaGroup& G = P.groups[g];
+            const int lt = t - G.tile_base;
+            const int m0 = (lt % G.tiles_m) * 2 * UM_BM + (int)rank * UM_BM, n0 = (lt / G.tiles_m) * G.bn;
+            u_mbar_wait(u_smem(&tfull[acc]), aph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int row = m0 + q * 32 + lane;
+            for (int c0 = 0; c0 < G.bn; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * UM_BN_MAX + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < G.M) {
+                    const int cb = n0 + c0;
+                    const int valid = min(32, min(G.bn - c0, G.N - cb));
+                    if (G.out_bf16) {
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(G.out) + (long long)row * G.ldo + cb;
+                        if (valid == 32 && ((G.ldo & 7) == 0)) {
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                uint4 w;
+                                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
+                                                                             __uint_as_float(r[v * 8 + 2 * e + 1]));
+                                    wp[e] = *reinterpret_cast<uint32_t*>(&h);
+                                }
+                                *reinterpret_cast<uint4*>(o + v * 8) = w;
+                            }
+                        } else {
+                            for (int e = 0; e < valid; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+                        }
+                    } else {
+                        float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
+                        if (valid == 32 && ((G.ldo & 3) == 0)) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v)
+                                *reinterpret_cast<float4*>(o + v * 4) =
+                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                        } else {
+                            for (int e = 0; e < valid; ++e) o[e] = __uint_as_float(r[e]);
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
+            if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -290,12 +507,24 @@ static int pick_bn(int N) {
     return std::min(bn, UM_BN_MAX);
 }
 
+static int umma_pairs_enabled() {
+    static const int v = [] {
+        const char* e = getenv("PG_UMMA_2CTA");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
         attr = true;
     }
+    // CTA pairs for batches whose every GEMM has at least 256 rows
+    bool pairs = umma_pairs_enabled() != 0;
+    for (const UmmaSpec& sp : specs) pairs = pairs && sp.M >= 2 * UM_BM;
     int dev = 0, sms = 0;
     PG_CUDA_THROW(cudaGetDevice(&dev));
     PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -309,15 +538,17 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
                 throw Error{PG_INVALID_ARGUMENT, "umma: operands need 16-byte aligned rows"};
             UmmaGroup& G = P->groups[g];
             G.bn = pick_bn(s.N);
+            if (pairs) G.bn = (G.bn + 31) / 32 * 32;  // each CTA of a pair loads bn/2 rows (multiple of 16)
+            if (G.bn > UM_BN_MAX) G.bn = UM_BN_MAX;
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
-            P->maps[2 * g + 1] = make_map(s.b, s.N, s.K, s.ldb, G.bn);
+            P->maps[2 * g + 1] = make_map(s.b, s.N, s.K, s.ldb, pairs ? G.bn / 2 : G.bn);
             G.out = s.out;
             G.ldo = s.ldo;
             G.M = s.M;
             G.N = s.N;
             G.K = s.K;
             G.out_bf16 = s.out_bf16;
-            G.tiles_m = (s.M + UM_BM - 1) / UM_BM;
+            G.tiles_m = (s.M + (pairs ? 2 * UM_BM : UM_BM) - 1) / (pairs ? 2 * UM_BM : UM_BM);
             G.tiles_n = (s.N + G.bn - 1) / G.bn;
             G.tile_base = tiles;
             tiles += G.tiles_m * G.tiles_n;
@@ -325,8 +556,44 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
         P->ngroups = ng;
         P->total_tiles = tiles;
         if (tiles == 0) continue;
-        k_umma_grouped<<<std::min(tiles, sms), UM_THREADS, UM_SMEM, st>>>(*P);
-        PG_LAUNCH_CHECK();
+        if (pairs) {
+            // persistent: only as many pairs as can be co-resident (cluster
+            // placement needs both SMs of a TPC free)
+            static int max_pairs = [&] {
+                cudaLaunchConfig_t q = {};
+                q.gridDim = dim3((unsigned)(sms / 2 * 2));
+                q.blockDim = dim3(UM_THREADS);
+                q.dynamicSmemBytes = U2_SMEM;
+                cudaLaunchAttribute a[1];
+                a[0].id = cudaLaunchAttributeClusterDimension;
+                a[0].val.clusterDim.x = 2;
+                a[0].val.clusterDim.y = 1;
+                a[0].val.clusterDim.z = 1;
+                q.attrs = a;
+                q.numAttrs = 1;
+                int n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, k_umma_grouped2, &q) != cudaSuccess || n <= 0) n = sms / 2;
+                if (getenv("PG_UMMA_DEBUG")) fprintf(stderr, "umma2: max active clusters %d (sms %d)\n", n, sms);
+                return n;
+            }();
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(2 * std::min(tiles, max_pairs)));
+            cfg.blockDim = dim3(UM_THREADS);
+            cfg.dynamicSmemBytes = U2_SMEM;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped2, *P));
+            count_launch();
+        } else {
+            k_umma_grouped<<<std::min(tiles, sms), UM_THREADS, UM_SMEM, st>>>(*P);
+            PG_LAUNCH_CHECK();
+        }
     }
 }
 
