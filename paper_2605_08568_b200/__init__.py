@@ -15,5 +15,5 @@ from .api import (AccessTrace, AggregatedLayer, CacheEntry, ColRange, ExecEngine
                   maximal_runs, mean_pool, retrieve, retrieve_device, rng_gaussian, route_select, route_select_pooled,
                   scattered_forward, score, silu_mul, copy_io, prefill_batched, module_forward, mlp_forward, select_topk, single_layer_k, store_rank, tensor_id,
                   variant_aggregated, variant_fused)
-from . import dist, embed, loaders  # noqa: F401,E402
+from . import dist, embed, loaders, train  # noqa: F401,E402
 from .loaders import load_cache, load_factorized  # noqa: F401,E402
