@@ -94,6 +94,74 @@ __device__ __forceinline__ void u_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+
+// ---- epilogue helpers: TMEM -> registers -> bf16 / f32 -> global, with the
+// next chunk's tcgen05.ld in flight while the current chunk is stored
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void store_chunk(const UmmaGroup& G, int row, int n0, int c0, const uint32_t (&r)[32]) {
+    if (row >= G.M) return;
+    const int cb = n0 + c0;
+    // columns of THIS tile only: the tile may be narrower than a 32-column chunk
+    const int valid = min(32, min(G.bn - c0, G.N - cb));
+    if (G.out_bf16) {
+        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(G.out) + (long long)row * G.ldo + cb;
+        if (valid == 32 && ((G.ldo & 7) == 0)) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                uint4 w;
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
+                                                             __uint_as_float(r[v * 8 + 2 * e + 1]));
+                    wp[e] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                *reinterpret_cast<uint4*>(o + v * 8) = w;
+            }
+        } else {
+            for (int e = 0; e < valid; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+        }
+    } else {
+        float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
+        if (valid == 32 && ((G.ldo & 3) == 0)) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+                *reinterpret_cast<float4*>(o + v * 4) = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                                    __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+        } else {
+            for (int e = 0; e < valid; ++e) o[e] = __uint_as_float(r[e]);
+        }
+    }
+}
+// one accumulator tile: lanes of quadrant q, columns [0, bn) in 32-column chunks
+__device__ __forceinline__ void epilogue_tile(const UmmaGroup& G, uint32_t tbase, int q, int row, int n0) {
+    const int nch = (G.bn + 31) / 32;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
+    uint32_t ra[32], rb[32];
+    tmem_ld32(lane_base, ra);
+    for (int c = 0; c < nch; c += 2) {
+        tmem_wait_ld();
+        if (c + 1 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 1)), rb);
+        store_chunk(G, row, n0, 32 * c, ra);
+        if (c + 1 >= nch) break;
+        tmem_wait_ld();
+        if (c + 2 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 2)), ra);
+        store_chunk(G, row, n0, 32 * (c + 1), rb);
+    }
+}
+
 __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_constant__ UmmaParams P) {
     extern __shared__ __align__(1024) unsigned char usmem[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(usmem) + 1023) & ~uintptr_t(1023));
@@ -192,55 +260,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
-            for (int c0 = 0; c0 < G.bn; c0 += 32) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * UM_BN_MAX + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < G.M) {
-                    const int cb = n0 + c0;
-                    // columns of THIS tile only: the tile may be narrower than a 32-column chunk
-                    const int valid = min(32, min(G.bn - c0, G.N - cb));
-                    if (G.out_bf16) {
-                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(G.out) + (long long)row * G.ldo + cb;
-                        if (valid == 32 && ((G.ldo & 7) == 0)) {
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                uint4 w;
-                                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
-                                                                             __uint_as_float(r[v * 8 + 2 * e + 1]));
-                                    wp[e] = *reinterpret_cast<uint32_t*>(&h);
-                                }
-                                *reinterpret_cast<uint4*>(o + v * 8) = w;
-                            }
-                        } else {
-                            for (int e = 0; e < valid; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
-                        }
-                    } else {
-                        float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
-                        if (valid == 32 && ((G.ldo & 3) == 0)) {
-#pragma unroll
-                            for (int v = 0; v < 8; ++v)
-                                *reinterpret_cast<float4*>(o + v * 4) =
-                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-                        } else {
-                            for (int e = 0; e < valid; ++e) o[e] = __uint_as_float(r[e]);
-                        }
-                    }
-                }
-            }
+            epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive(u_smem(&tempty[acc]));
@@ -408,54 +428,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
-            for (int c0 = 0; c0 < G.bn; c0 += 32) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * UM_BN_MAX + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                      "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                      "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                      "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < G.M) {
-                    const int cb = n0 + c0;
-                    const int valid = min(32, min(G.bn - c0, G.N - cb));
-                    if (G.out_bf16) {
-                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(G.out) + (long long)row * G.ldo + cb;
-                        if (valid == 32 && ((G.ldo & 7) == 0)) {
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) {
-                                uint4 w;
-                                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
-                                                                             __uint_as_float(r[v * 8 + 2 * e + 1]));
-                                    wp[e] = *reinterpret_cast<uint32_t*>(&h);
-                                }
-                                *reinterpret_cast<uint4*>(o + v * 8) = w;
-                            }
-                        } else {
-                            for (int e = 0; e < valid; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
-                        }
-                    } else {
-                        float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
-                        if (valid == 32 && ((G.ldo & 3) == 0)) {
-#pragma unroll
-                            for (int v = 0; v < 8; ++v)
-                                *reinterpret_cast<float4*>(o + v * 4) =
-                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-                        } else {
-                            for (int e = 0; e < valid; ++e) o[e] = __uint_as_float(r[e]);
-                        }
-                    }
-                }
-            }
+            epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));

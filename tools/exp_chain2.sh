@@ -1,3 +1,3 @@
 O=gpurun_out; mkdir -p $O
-for R in 1 4; do echo "R=$R"; PG_CHAIN_DBG=1 EXP_ONLY=mlp timeout 120 python tools/exp_decode.py $R 512; done > $O/ec2.txt 2>&1
+for ns in 0 20 50 100 200 400; do echo "pollns $ns"; PG_CHAIN_POLLNS=$ns EXP_ONLY=mlp timeout 120 python tools/exp_decode.py 4 2048; done > $O/ec2.txt 2>&1
 cat $O/ec2.txt
