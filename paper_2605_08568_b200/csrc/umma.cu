@@ -50,6 +50,7 @@ struct UmmaGroup {
 // tensor maps straight from parameter space, no staging copy.
 struct __align__(64) UmmaParams {
     CUtensorMap maps[2 * UM_MAX_GROUPS];  // [2g] A [M rows, K] box {64,128}; [2g+1] B [N rows, K] box {64,BN}
+    CUtensorMap omaps[UM_MAX_GROUPS];     // output [M rows, N] box {32, 32} (TMA-store epilogue of the pair kernel)
     UmmaGroup groups[UM_MAX_GROUPS];
     int ngroups;
     int total_tiles;
@@ -283,7 +284,8 @@ constexpr int U2_STAGES = 6;
 constexpr int U2_A_BYTES = UM_BM * UM_BK * 2;                 // 16 KB (this CTA's 128 rows)
 constexpr int U2_B_BYTES = (UM_BN_MAX / 2) * UM_BK * 2;       // 16 KB (this CTA's BN/2 rows)
 constexpr int U2_STAGE_BYTES = U2_A_BYTES + U2_B_BYTES;
-constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 256;
+constexpr int U2_OUT_BYTES = 32 * 32 * 4;  // one 32 x 32 output chunk (f32 worst case)
+constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 256 + 4 * 2 * U2_OUT_BYTES;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -324,6 +326,69 @@ __device__ __forceinline__ void u_commit2(uint32_t bar) {  // arrive on this bar
         " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}"
         ::"r"(bar)
         : "memory");
+}
+
+
+// TMA-store epilogue: each warp stages its 32 rows x 32 columns in shared
+// memory (double-buffered) and one lane stores the box with
+// cp.async.bulk.tensor -- coalesced rows instead of one row per thread.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
+                 "r"(y), "r"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUtensorMap* omap, uint32_t tbase, int q,
+                                                  int lane, int row0, int n0, unsigned char* stage, int& nbuf) {
+    const int nch = (G.bn + 31) / 32;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
+    const int es = G.out_bf16 ? 2 : 4;
+    uint32_t ra[32], rb[32];
+    auto emit = [&](int c, const uint32_t (&r)[32]) {
+        const int c0 = 32 * c;
+        if (c0 + 32 > G.bn) {  // partial chunk: the box would spill into the next tile
+            store_chunk(G, row0 + lane, n0, c0, r);
+            return;
+        }
+        unsigned char* buf = stage + (nbuf & 1) * U2_OUT_BYTES;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buf's previous store read it
+        __syncwarp();
+        unsigned char* dst = buf + lane * 32 * es;
+        if (G.out_bf16) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                uint4 w;
+                uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
+                                                             __uint_as_float(r[v * 8 + 2 * e + 1]));
+                    wp[e] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                *reinterpret_cast<uint4*>(dst + v * 16) = w;
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+                *reinterpret_cast<uint4*>(dst + v * 16) = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(omap, u_smem(buf), n0 + c0, row0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        ++nbuf;
+    };
+    tmem_ld32(lane_base, ra);
+    for (int c = 0; c < nch; c += 2) {
+        tmem_wait_ld();
+        if (c + 1 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 1)), rb);
+        emit(c, ra);
+        if (c + 1 >= nch) break;
+        tmem_wait_ld();
+        if (c + 2 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 2)), ra);
+        emit(c + 1, rb);
+    }
 }
 
 __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_constant__ UmmaParams P) {
@@ -417,6 +482,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
     } else {
         // ------------------------------------------------ epilogue (warps 2-5, both CTAs)
         const int q = warp & 3;
+        unsigned char* ostage = base + U2_STAGES * U2_STAGE_BYTES + 1024 + (q) * 2 * U2_OUT_BYTES;
+        int nbuf = 0;
         int acc = 0;
         uint32_t aph = 0;
         for (int t = pair; t < P.total_tiles; t += npairs) {
@@ -428,13 +495,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
-            epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
+            epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
             if (++acc == 2) { acc = 0; aph ^= 1; }
         }
     }
+    if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores out of smem
     asm volatile("tcgen05.fence::before_thread_sync;");
     cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -473,6 +541,19 @@ static CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int 
     return m;
 }
 
+static CUtensorMap make_out_map(void* ptr, int rows, int cols, long long ld, bool bf16) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * (bf16 ? 2 : 4)};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = get_encode()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr,
+                                    dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error{PG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (output)"};
+    return m;
+}
+
 static int pick_bn(int N) {
     const int tiles = (N + UM_BN_MAX - 1) / UM_BN_MAX;
     int bn = (N + tiles - 1) / tiles;
@@ -497,7 +578,9 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
     }
     // CTA pairs for batches whose every GEMM has at least 256 rows
     bool pairs = umma_pairs_enabled() != 0;
-    for (const UmmaSpec& sp : specs) pairs = pairs && sp.M >= 2 * UM_BM;
+    for (const UmmaSpec& sp : specs)  // (+ 16-byte aligned output rows for the TMA-store epilogue)
+        pairs = pairs && sp.M >= 2 * UM_BM && (sp.ldo * (sp.out_bf16 ? 2 : 4)) % 16 == 0 &&
+                reinterpret_cast<uintptr_t>(sp.out) % 16 == 0;
     int dev = 0, sms = 0;
     PG_CUDA_THROW(cudaGetDevice(&dev));
     PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -515,6 +598,7 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             if (G.bn > UM_BN_MAX) G.bn = UM_BN_MAX;
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
             P->maps[2 * g + 1] = make_map(s.b, s.N, s.K, s.ldb, pairs ? G.bn / 2 : G.bn);
+            if (pairs) P->omaps[g] = make_out_map(s.out, s.M, s.N, s.ldo, s.out_bf16 != 0);
             G.out = s.out;
             G.ldo = s.ldo;
             G.M = s.M;
