@@ -163,6 +163,7 @@ def build_block(pg, torch, sh, dev, seed):
         sig = 1.0 / (1.0 + torch.arange(r, device=dev, dtype=torch.float32) / 64.0)
         a = (torch.randn((m, r), generator=g, device=dev) * sig / m ** 0.5).to(torch.bfloat16)
         layers[name] = pg.FactorizedLayer.from_device(bt, a, K, layer_id=name)
+        layers[name]._raw = (bt, a, K)  # for the native fixed-rank SVD baseline
     return layers
 
 
@@ -271,6 +272,55 @@ def gpu_arm(args, rank, world, local_rank):
             ms = float(t.item())
         return ms, reps * G
 
+    # ---- baselines in the same run: native fixed-rank SVD, i.e.
+    # the static prefix A[:, :K] (B[:, :K]^T x) through cuBLAS (torch.matmul),
+    # and the dense layer W x, both bf16, same replicas, same graph recipe
+    def cublas_graph(mats):
+        xb = torch.randn((G, D_MODEL), generator=gen, device=dev).to(torch.bfloat16)
+
+        def one(i):
+            w = mats[i % REPLICAS]
+            if len(w) == 6:  # fixed-rank SVD: B_K^T x then A_K z per linear
+                bu, au, bg, ag, bd, ad = w
+                u = au @ (bu @ xb[i])
+                gg = ag @ (bg @ xb[i])
+                return ad @ (bd @ (torch.nn.functional.silu(gg) * u))
+            wu, wg, wd = w
+            return wd @ (torch.nn.functional.silu(wg @ xb[i]) * (wu @ xb[i]))
+
+        with torch.cuda.stream(stream):
+            for i in range(G):
+                one(i)
+        stream.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            for i in range(G):
+                one(i)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            gr.replay()
+            s0.record(stream)
+            for _ in range(8):
+                gr.replay()
+            s1.record(stream)
+        torch.cuda.synchronize()
+        return 8 * G / (s0.elapsed_time(s1) * 1e-3) * world
+
+    svd = []
+    for b in blocks:
+        w = []
+        for nm in ("up", "gate", "down"):
+            bt, a, K_ = b[nm]._raw
+            w += [bt[:K_].contiguous(), a[:, :K_].contiguous()]
+        svd.append(tuple(w))
+    svd_tok_s = cublas_graph(svd)
+    del svd
+    dense = [tuple(torch.randn(shp, generator=gen, device=dev).to(torch.bfloat16) / 64
+                   for shp in ((D_FF, D_MODEL), (D_FF, D_MODEL), (D_MODEL, D_FF))) for _ in range(REPLICAS)]
+    dense_tok_s = cublas_graph(dense)
+    del dense
+    torch.cuda.empty_cache()
+
     with ClockSampler(local_rank) as clk:
         ms, nsteps = timed(False, args.steps)
     ms_e2e, nsteps_e2e = timed(True, args.steps)
@@ -281,6 +331,10 @@ def gpu_arm(args, rank, world, local_rank):
     # fused MLP block; one launch per step, timed by CUDA events on its stream
     # over the timed region.  Algorithmic bytes = sum_l K_l (m_l + n_l) * 2 (the
     # selected experts' U and V rows) + x, act (write+read) and y.
+    traffic = None  # dram read+write bytes per launch of k_chain from the committed ncu --set full capture
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("k_chain<bf16>")
     lin_bytes = {k: K_ * (m_ + n_) * 2 for k, (m_, n_, K_, _) in sh.items()}
     step_bytes = sum(lin_bytes.values()) + D_MODEL * 2 + D_FF * 2 * 2 + D_MODEL * 4
     step_us = ms / nsteps * 1e3
@@ -300,7 +354,7 @@ def gpu_arm(args, rank, world, local_rank):
         "e2e": {"value": nsteps_e2e / (ms_e2e * 1e-3) * world, "unit": "tokens/s",
                 "h2d_bytes_per_step": D_MODEL * 2, "d2h_bytes_per_step": D_MODEL * 4},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": traffic,
                      "kernel": "k_chain<bf16> (fused MLP block: up+gate stage 1, grid barrier, stage 2 + "
                                "silu epilogue, down stage 1/2; 1 launch per step)",
                      "alg_bytes_per_launch": step_bytes, "avg_us": step_us, "peak_kind": peak_kind},
@@ -311,6 +365,9 @@ def gpu_arm(args, rank, world, local_rank):
         "gpu_launches": int(launches_per_step * nsteps),
         "clocks": clk.summary(),
         "prefill_setup": {"retrieve_us": retrieve_us, "retrieve_plus_pack_ms_host": setup_ms},
+        "baselines": {"native_fixed_rank_svd_cublas_tok_s": svd_tok_s, "dense_cublas_tok_s": dense_tok_s,
+                      "note": "static prefix A[:, :K](B[:, :K]^T x) and dense W x, bf16 torch.matmul, "
+                              "same replicas, CUDA graph of 64 steps"},
     }
     if args.prefill:
         del blocks, aggs
