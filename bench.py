@@ -373,7 +373,73 @@ def gpu_arm(args, rank, world, local_rank):
         del blocks, aggs
         torch.cuda.empty_cache()
         out["prefill"] = prefill_arm(pg, torch, dev, world)
+        torch.cuda.empty_cache()
+    if args.decode_batch:
+        out["decode_batch"] = decode_batch_arm(pg, torch, dev, world, hbm_peak)
     return out
+
+
+def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct=4):
+    """BASELINE config 4 (per GPU, data-parallel): a 32-layer LLaMA-7B-shaped
+    stack of rank-expert linears decoding 256 prompts x 1 token, each prompt
+    with its own selection per linear (the reference's pattern generator).
+    Union-masked: every linear reads its stored experts once for the whole
+    batch (two tcgen05 GEMMs, the per-token mask in the first's epilogue).
+    `distinct` layer weight sets (each 324 MB > L2) are cycled through the 32
+    layers; attention and norms are outside the path."""
+    lin = {"q": (D_MODEL, D_MODEL), "k": (D_MODEL, D_MODEL), "v": (D_MODEL, D_MODEL), "o": (D_MODEL, D_MODEL),
+           "up": (D_FF, D_MODEL), "gate": (D_FF, D_MODEL), "down": (D_MODEL, D_FF)}
+    dims = [(pg.store_rank(pg.single_layer_k(m, n, RATIO), n), pg.single_layer_k(m, n, RATIO)) for m, n in lin.values()]
+    pats = pg.make_patterns(17171, P, dims)  # the reference's generator (pg_make_patterns, same bits)
+    g = torch.Generator(device=dev).manual_seed(11)
+    stack = []
+    for _ in range(distinct):
+        lay = {}
+        for li, (nm, (m, n)) in enumerate(lin.items()):
+            r, K = dims[li]
+            bt = (torch.randn(r, n, device=dev, generator=g) / n ** 0.5).to(torch.bfloat16)
+            a = (torch.randn(m, r, device=dev, generator=g) / m ** 0.5).to(torch.bfloat16)
+            L = pg.FactorizedLayer.from_device(bt, a, K, layer_id=nm)
+            lay[nm] = (L, pg.SelectionBatch(L, [p[li] for p in pats]))
+        stack.append(lay)
+    X = {n: torch.randn(P, n, device=dev, generator=g).to(torch.bfloat16) for n in (D_MODEL, D_FF)}
+    Y = {m: torch.empty(P, m, device=dev, dtype=torch.bfloat16) for m in (D_MODEL, D_FF)}
+    tp = torch.arange(P, device=dev, dtype=torch.int32)  # prompt q -> its own selection q
+
+    def step():
+        for li in range(layers):
+            for nm, (m, n) in lin.items():
+                L, sb = stack[li % distinct][nm]
+                pg.masked_forward_union(L, sb, tp, X[n], out_dtype=torch.bfloat16, out=Y[m])
+
+    st = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(st):
+        step()
+    st.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    n0 = pg.launch_count()
+    with torch.cuda.graph(gr, stream=st):
+        step()
+    launches = pg.launch_count() - n0
+    reps = 5
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        gr.replay()
+        e0.record(st)
+        for _ in range(reps):
+            gr.replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    byt = layers * sum(dims[i][0] * (m + n) * 2 for i, (m, n) in enumerate(lin.values()))
+    fl = layers * 2 * P * sum(dims[i][0] * (m + n) for i, (m, n) in enumerate(lin.values()))
+    return {"workload": f"config4: {layers}-layer LLaMA-7B-shaped stack, {P} prompts x 1 decode token, "
+                        f"{P} heterogeneous selections per linear (reference generator, seed 17171), "
+                        f"union-masked tcgen05 GEMMs; {distinct} distinct layer weight sets cycled (each > L2)",
+            "tokens_per_s": P / (ms * 1e-3) * world, "ms_per_step": ms, "launches_per_step": launches,
+            "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": byt / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": byt,
+                         "tensor_tflops": fl / (ms * 1e-3) / 1e12}}
 
 
 def prefill_arm(pg, torch, dev, world, P=16, T=2048):
@@ -462,6 +528,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--prefill", type=int, default=1, help="also measure config-3 prefill (secondary)")
+    ap.add_argument("--decode-batch", type=int, default=1,
+                    help="also measure config-4 batched heterogeneous decode (secondary)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -219,6 +219,20 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns_h
                    const int32_t* pattern_dev, const void* x_dev, void* act_dev, void* y_dev,
                    pg_dtype y_dtype, pg_stream stream);
 
+/* Union-masked heterogeneous batch (BASELINE config 4: decode batch of
+ * prompts, each with its own selection): masked_forward (rank_experts.hpp:52-72)
+ * for every token t of token-major x [T, n] with the selection of pattern
+ * tok_pat_dev[t], reading the layer's weights once for the whole batch (two
+ * tcgen05 GEMMs over all r_store experts, non-selected experts zeroed per token
+ * in the first GEMM's epilogue).  bf16 layers; y token-major [T, m] (bf16/f32).
+ * masks_dev: [P, stride] bytes from pg_selection_masks (stride from
+ * pg_selection_mask_stride); tok_pat_dev values must lie in [0, P). */
+int pg_selection_mask_stride(pg_layer layer, size_t* stride);
+int pg_selection_masks(pg_layer layer, const uint32_t* sels_concat, const size_t* ks, size_t P,
+                       uint8_t* masks_dev, pg_stream stream);
+int pg_masked_forward_union(pg_layer layer, const uint8_t* masks_dev, size_t P, const int32_t* tok_pat_dev,
+                            size_t T, const void* x_dev, void* y_dev, pg_dtype y_dtype, pg_stream stream);
+
 /* Heterogeneous prefill (config 3): prompt p owns tokens
  * [offsets_host[p], offsets_host[p+1]) of token-major x (bf16) and its own
  * aggregated layout aggs[p] (served with pattern 0, e.g. the single pattern

@@ -422,6 +422,53 @@ def masked_forward(layer: FactorizedLayer, sel, x: torch.Tensor, layout: str = "
 
 
 @dataclass
+class SelectionBatch:
+    """P selections of one layer as device byte masks [P, stride]
+    (pg_selection_masks); each selection is validated like check_selection
+    (rank_experts.hpp:30-37)."""
+
+    def __init__(self, layer: FactorizedLayer, selections):
+        sels = [np.ascontiguousarray(s.indices if isinstance(s, RankSelection) else s, dtype=np.uint32)
+                for s in selections]
+        if not sels:
+            raise ValueError("selection batch: no selections")
+        stride = C.c_size_t()
+        call("pg_selection_mask_stride", layer.handle, C.byref(stride))
+        self.layer, self.P, self.stride = layer, len(sels), stride.value
+        self.masks = torch.zeros(self.P * self.stride, dtype=torch.uint8, device="cuda")
+        flat = np.ascontiguousarray(np.concatenate(sels))
+        ks = (C.c_size_t * self.P)(*[s.size for s in sels])
+        call("pg_selection_masks", layer.handle, flat.ctypes.data_as(C.POINTER(C.c_uint32)), ks, self.P,
+             _ptr(self.masks), _stream())
+
+
+def masked_forward_union(layer: FactorizedLayer, batch: SelectionBatch, token_patterns, x: torch.Tensor,
+                         out_dtype=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """masked_forward (rank_experts.hpp:52-72) for every token of a heterogeneous
+    token-major batch x [T, n]: token t uses selection token_patterns[t] of
+    `batch`.  The weights are read once for the whole batch (config 4)."""
+    if batch.layer is not layer:
+        raise ValueError("masked_forward_union: selection batch built for another layer")
+    x = _dev(x, torch.bfloat16)
+    if x.dim() != 2 or x.shape[1] != layer.n:
+        raise ValueError("masked_forward_union: bad X shape")
+    T = x.shape[0]
+    if isinstance(token_patterns, torch.Tensor) and token_patterns.is_cuda:
+        tp = token_patterns.to(torch.int32).contiguous()  # device ids are trusted
+    else:
+        tpn = np.ascontiguousarray(token_patterns, dtype=np.int64)
+        if tpn.size and (tpn.min() < 0 or tpn.max() >= batch.P):
+            raise IndexError("masked_forward_union: unknown pattern")
+        tp = torch.from_numpy(tpn.astype(np.int32)).cuda()
+    if tp.numel() != T:
+        raise ValueError("masked_forward_union: one pattern id per token")
+    ydt = _out_dtype(layer.dtype, out_dtype)
+    y = out if out is not None else torch.empty((T, layer.m), dtype=_TORCH[ydt], device=x.device)
+    call("pg_masked_forward_union", layer.handle, _ptr(batch.masks), batch.P, _ptr(tp), T, _ptr(x), _ptr(y), ydt,
+         _stream())
+    return y
+
+
 class AccessTrace:
     """exec_engine.hpp:90-92."""
     a_cols: list = field(default_factory=list)

@@ -815,6 +815,66 @@ int pg_masked_forward(pg_layer L, const uint32_t* sel, size_t k, int sel_on_dev,
     PG_API_END
 }
 
+// ------------------------------------------------------------ union-masked batches
+// Heterogeneous decode batches (BASELINE config 4): every token t carries its
+// prompt's selection S_p(t).  Rather than one pass over the weights per prompt,
+// the union of the selections -- all r_store experts once a GPU serves more than
+// a handful of patterns -- is read ONCE for the whole batch:
+//   Z[T, r] = X[T, n] . B^T[r, n]^T, masked per row: Z[t, e] = 0 unless e in S_p(t)
+//   Y[T, m] = Z[T, r] . A[m, r]^T
+// which is masked_forward (rank_experts.hpp:52-72) for every token: the masked
+// experts contribute exact zeros.  Both stages are tcgen05 GEMMs; the mask is
+// applied in the stage-1 epilogue (per-row pattern id -> [P, ld] byte mask).
+static size_t sel_mask_ld(int r) { return round_up((size_t)r + 32, 64); }
+
+int pg_selection_mask_stride(pg_layer L, size_t* out) {
+    PG_API_BEGIN
+    require(L && out, PG_INVALID_ARGUMENT, "selection_mask_stride: bad arguments");
+    *out = sel_mask_ld(L->r);
+    PG_API_END
+}
+
+int pg_selection_masks(pg_layer L, const uint32_t* sels, const size_t* ks, size_t P, uint8_t* masks, pg_stream s) {
+    PG_API_BEGIN
+    require(L && sels && ks && masks && P > 0, PG_INVALID_ARGUMENT, "selection_masks: bad arguments");
+    const size_t ld = sel_mask_ld(L->r);
+    std::vector<uint8_t> h(P * ld, 0);
+    size_t off = 0;
+    for (size_t p = 0; p < P; ++p) {
+        check_sel_host(sels + off, ks[p], (size_t)L->r);
+        for (size_t q = 0; q < ks[p]; ++q) h[p * ld + sels[off + q]] = 1;
+        off += ks[p];
+    }
+    const cudaStream_t st = as_stream(s);
+    PG_CUDA_THROW(cudaMemcpyAsync(masks, h.data(), h.size(), cudaMemcpyHostToDevice, st));
+    PG_CUDA_THROW(cudaStreamSynchronize(st));
+    PG_API_END
+}
+
+int pg_masked_forward_union(pg_layer L, const uint8_t* masks, size_t P, const int32_t* tok_pat, size_t T,
+                            const void* x, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(L && masks && tok_pat && x && y && P > 0 && T > 0, PG_INVALID_ARGUMENT,
+            "masked_forward_union: bad arguments");
+    require(L->dt == PG_BF16, PG_INVALID_ARGUMENT, "masked_forward_union: bf16 layers (tensor-core path)");
+    require(L->n % 8 == 0, PG_INVALID_ARGUMENT, "masked_forward_union: n must be a multiple of 8");
+    check_ydt(L->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const int rp = (int)round_up((size_t)L->r, 8);
+    Scratch z((size_t)T * rp * 2, st);
+    // tokens on M, experts on N (narrow tiles cover the SMs, launch_umma);
+    // measured: this beats K split across CTAs (f32 partials outweigh the
+    // weights at T = 256) and the weights-on-M orientation
+    UmmaSpec s1{x, L->n, L->bt, L->ldb, z.p, rp, (int)T, rp, L->n, 1};
+    s1.mask = masks;
+    s1.mask_ld = (long long)sel_mask_ld(L->r);
+    s1.row_pat = tok_pat;
+    s1.b_rows = L->r;
+    launch_umma({s1}, st);
+    launch_umma({UmmaSpec{z.p, rp, L->a, L->lda, y, L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0}}, st);
+    PG_API_END
+}
+
 // ------------------------------------------------------------ aggregated layout
 int pg_aggregate_layout(pg_agg* out, pg_layer L, const uint32_t* pats, const size_t* ks, size_t P,
                         double psi, pg_stream s) {

@@ -484,7 +484,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == kConsumerWarps) {
         // weights are immutable: the producer never waits on the previous grid
-        if (lane == 0) chain_producer<W>(P, lins, descs, full, empty, ring, nst);
+        if (lane == 0) {
+            chain_producer<W>(P, lins, descs, full, empty, ring, nst);
+            if (P.dbg) P.dbg[blockIdx.x * 16 + 12] = gtimer();  // every copy issued
+        }
         return;
     }
     // launch tag: every CTA adds 1 to the workspace's epoch counter before it
@@ -707,6 +710,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         STAMP(ph * 6 + 5);
         if (ph + 1 < P.nphase) grid_sync_consumers(P.bar);  // act complete before phase ph+1 reads it
     }
+    STAMP(13);
 }
 
 static int g_num_sms = 0;

@@ -44,6 +44,9 @@ struct UmmaGroup {
     int out_bf16;              // 1: bf16 out, 0: f32 out
     int tiles_m, tiles_n;
     int tile_base;             // prefix sum of tiles over groups
+    const uint8_t* mask;       // nullable: per-row column mask (see UmmaSpec)
+    long long mask_ld;
+    const int32_t* row_pat;
 };
 
 // Passed as one __grid_constant__ parameter block (< 32 KB): TMA reads the
@@ -146,6 +149,20 @@ __device__ __forceinline__ void store_chunk(const UmmaGroup& G, int row, int n0,
         }
     }
 }
+// union-masked batches: zero the columns this row's pattern does not select
+// (32 mask bytes per chunk, two 16-byte loads; mask_ld >= N rounded up + 32)
+__device__ __forceinline__ void mask_chunk(const UmmaGroup& G, int row, int col0, uint32_t (&r)[32]) {
+    if (G.mask == nullptr) return;
+    if (row >= G.M) return;
+    const uint8_t* mr = G.mask + (long long)__ldg(G.row_pat + row) * G.mask_ld + col0;
+    const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(mr));
+    const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(mr + 16));
+    const uint32_t w[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+        if (((w[e >> 2] >> (8 * (e & 3))) & 0xFFu) == 0) r[e] = 0u;
+}
+
 // one accumulator tile: lanes of quadrant q, columns [0, bn) in 32-column chunks
 __device__ __forceinline__ void epilogue_tile(const UmmaGroup& G, uint32_t tbase, int q, int row, int n0) {
     const int nch = (G.bn + 31) / 32;
@@ -155,10 +172,12 @@ __device__ __forceinline__ void epilogue_tile(const UmmaGroup& G, uint32_t tbase
     for (int c = 0; c < nch; c += 2) {
         tmem_wait_ld();
         if (c + 1 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 1)), rb);
+        mask_chunk(G, row, n0 + 32 * c, ra);
         store_chunk(G, row, n0, 32 * c, ra);
         if (c + 1 >= nch) break;
         tmem_wait_ld();
         if (c + 2 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 2)), ra);
+        mask_chunk(G, row, n0 + 32 * (c + 1), rb);
         store_chunk(G, row, n0, 32 * (c + 1), rb);
     }
 }
@@ -343,8 +362,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUte
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const int es = G.out_bf16 ? 2 : 4;
     uint32_t ra[32], rb[32];
-    auto emit = [&](int c, const uint32_t (&r)[32]) {
+    auto emit = [&](int c, uint32_t (&r)[32]) {
         const int c0 = 32 * c;
+        mask_chunk(G, row0 + lane, n0 + c0, r);
         if (c0 + 32 > G.bn) {  // partial chunk: the box would spill into the next tile
             store_chunk(G, row0 + lane, n0, c0, r);
             return;
@@ -596,8 +616,32 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             G.bn = pick_bn(s.N);
             if (pairs) G.bn = (G.bn + 31) / 32 * 32;  // each CTA of a pair loads bn/2 rows (multiple of 16)
             if (G.bn > UM_BN_MAX) G.bn = UM_BN_MAX;
+            if (s.bn > 0) {
+                G.bn = s.bn;
+            } else if (ng == 1 && (long)((s.M + (pairs ? 2 * UM_BM : UM_BM) - 1) / (pairs ? 2 * UM_BM : UM_BM)) *
+                                   ((s.N + G.bn - 1) / G.bn) < (pairs ? sms / 2 : sms)) {
+                // a lone GEMM with few tiles (small-batch decode through the
+                // tensor cores): narrower tiles until the SMs are covered,
+                // minimising waves x tile width (time per tile ~ bn x K)
+                const int rows = pairs ? 2 * UM_BM : UM_BM;
+                const int slots = pairs ? sms / 2 : sms;
+                const int tm = (s.M + rows - 1) / rows;
+                const int step = pairs ? 32 : 16;
+                long best = -1;
+                int best_bn = G.bn;
+                for (int bn = G.bn; bn >= step; bn -= step) {
+                    const long tiles_b = (long)tm * ((s.N + bn - 1) / bn);
+                    const long cost = ((tiles_b + slots - 1) / slots) * (long)bn;
+                    if (best < 0 || cost < best) { best = cost; best_bn = bn; }
+                }
+                G.bn = best_bn;
+            }
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
-            P->maps[2 * g + 1] = make_map(s.b, s.N, s.K, s.ldb, pairs ? G.bn / 2 : G.bn);
+            P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
+                                          pairs ? G.bn / 2 : G.bn);
+            G.mask = s.mask;
+            G.mask_ld = s.mask_ld;
+            G.row_pat = s.row_pat;
             if (pairs) P->omaps[g] = make_out_map(s.out, s.M, s.N, s.ldo, s.out_bf16 != 0);
             G.out = s.out;
             G.ldo = s.ldo;
