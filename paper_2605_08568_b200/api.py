@@ -421,7 +421,6 @@ def masked_forward(layer: FactorizedLayer, sel, x: torch.Tensor, layout: str = "
     return y
 
 
-@dataclass
 class SelectionBatch:
     """P selections of one layer as device byte masks [P, stride]
     (pg_selection_masks); each selection is validated like check_selection
@@ -469,6 +468,7 @@ def masked_forward_union(layer: FactorizedLayer, batch: SelectionBatch, token_pa
     return y
 
 
+@dataclass
 class AccessTrace:
     """exec_engine.hpp:90-92."""
     a_cols: list = field(default_factory=list)
