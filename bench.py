@@ -403,14 +403,17 @@ def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct
             lay[nm] = (L, pg.SelectionBatch(L, [p[li] for p in pats]))
         stack.append(lay)
     X = {n: torch.randn(P, n, device=dev, generator=g).to(torch.bfloat16) for n in (D_MODEL, D_FF)}
-    Y = {m: torch.empty(P, m, device=dev, dtype=torch.bfloat16) for m in (D_MODEL, D_FF)}
     tp = torch.arange(P, device=dev, dtype=torch.int32)  # prompt q -> its own selection q
+
+    Yl = {nm: torch.empty(P, m, device=dev, dtype=torch.bfloat16) for nm, (m, n) in lin.items()}
+    groups = (("q", "k", "v"), ("o",), ("up", "gate"), ("down",))  # linears sharing an input: one launch per stage
 
     def step():
         for li in range(layers):
-            for nm, (m, n) in lin.items():
-                L, sb = stack[li % distinct][nm]
-                pg.masked_forward_union(L, sb, tp, X[n], out_dtype=torch.bfloat16, out=Y[m])
+            lay = stack[li % distinct]
+            for grp in groups:
+                pg.module_forward_union([lay[g][0] for g in grp], [lay[g][1] for g in grp], tp, X[lin[grp[0]][1]],
+                                        out_dtype=torch.bfloat16, outs=[Yl[g] for g in grp])
 
     st = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(st):
@@ -435,7 +438,8 @@ def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct
     fl = layers * 2 * P * sum(dims[i][0] * (m + n) for i, (m, n) in enumerate(lin.values()))
     return {"workload": f"config4: {layers}-layer LLaMA-7B-shaped stack, {P} prompts x 1 decode token, "
                         f"{P} heterogeneous selections per linear (reference generator, seed 17171), "
-                        f"union-masked tcgen05 GEMMs; {distinct} distinct layer weight sets cycled (each > L2)",
+                        f"union-masked tcgen05 GEMMs (q/k/v and up/gate grouped per stage); {distinct} distinct layer "
+                        f"weight sets cycled (each > L2)",
             "tokens_per_s": P / (ms * 1e-3) * world, "ms_per_step": ms, "launches_per_step": launches,
             "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": byt / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": byt,

@@ -232,6 +232,12 @@ int pg_selection_masks(pg_layer layer, const uint32_t* sels_concat, const size_t
                        uint8_t* masks_dev, pg_stream stream);
 int pg_masked_forward_union(pg_layer layer, const uint8_t* masks_dev, size_t P, const int32_t* tok_pat_dev,
                             size_t T, const void* x_dev, void* y_dev, pg_dtype y_dtype, pg_stream stream);
+/* The same for 1..32 linears sharing the input x (q/k/v, up/gate): each
+ * stage is one grouped launch over all linears.  masks_dev[l] / P[l] per
+ * linear (pg_selection_masks of that layer), one pattern id per token. */
+int pg_module_forward_union(const pg_layer* layers, const uint8_t* const* masks_dev, const size_t* P,
+                            size_t n_linears, const int32_t* tok_pat_dev, size_t T, const void* x_dev,
+                            void* const* ys_dev, pg_dtype y_dtype, pg_stream stream);
 
 /* Heterogeneous prefill (config 3): prompt p owns tokens
  * [offsets_host[p], offsets_host[p+1]) of token-major x (bf16) and its own

@@ -80,6 +80,7 @@ _SIGS = {
     "pg_selection_mask_stride": [_vp, _vp],
     "pg_selection_masks": [_vp, _vp, _vp, _sz, _vp, _vp],
     "pg_masked_forward_union": [_vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],
+    "pg_module_forward_union": [_vp, _vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],
     "pg_module_forward": [C.POINTER(_vp), _sz, _sp, _vp, _vp, C.POINTER(_vp), _i, _vp],
     "pg_prefill_batched": [C.POINTER(_vp), _i64p, _sz, _vp, _vp, _i, _vp],
     "pg_gemm_bf16": [_vp, C.c_int64, _vp, C.c_int64, _vp, C.c_int64, _sz, _sz, _sz, _i, _vp],

@@ -468,6 +468,36 @@ def masked_forward_union(layer: FactorizedLayer, batch: SelectionBatch, token_pa
     return y
 
 
+def module_forward_union(layers, batches, token_patterns, x: torch.Tensor, out_dtype=None, outs=None) -> list:
+    """masked_forward_union for several linears sharing x (q/k/v or up/gate):
+    one grouped launch per stage over all of them."""
+    if len(layers) != len(batches) or not layers:
+        raise ValueError("module_forward_union: one selection batch per layer")
+    for L, b in zip(layers, batches):
+        if b.layer is not L:
+            raise ValueError("module_forward_union: selection batch built for another layer")
+    x = _dev(x, torch.bfloat16)
+    T = x.shape[0]
+    if isinstance(token_patterns, torch.Tensor) and token_patterns.is_cuda:
+        tp = token_patterns.to(torch.int32).contiguous()
+    else:
+        tpn = np.ascontiguousarray(token_patterns, dtype=np.int64)
+        if tpn.size and (tpn.min() < 0 or tpn.max() >= min(b.P for b in batches)):
+            raise IndexError("module_forward_union: unknown pattern")
+        tp = torch.from_numpy(tpn.astype(np.int32)).cuda()
+    if tp.numel() != T:
+        raise ValueError("module_forward_union: one pattern id per token")
+    ydt = _out_dtype(layers[0].dtype, out_dtype)
+    ys = outs if outs is not None else [torch.empty((T, L.m), dtype=_TORCH[ydt], device=x.device) for L in layers]
+    n = len(layers)
+    hs = (C.c_void_p * n)(*[L.handle.value if hasattr(L.handle, "value") else L.handle for L in layers])
+    ms = (C.c_void_p * n)(*[_ptr(b.masks) for b in batches])
+    ps = (C.c_size_t * n)(*[b.P for b in batches])
+    yp = (C.c_void_p * n)(*[_ptr(y) for y in ys])
+    call("pg_module_forward_union", hs, ms, ps, n, _ptr(tp), T, _ptr(x), yp, ydt, _stream())
+    return ys
+
+
 @dataclass
 class AccessTrace:
     """exec_engine.hpp:90-92."""

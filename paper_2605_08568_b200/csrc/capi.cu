@@ -875,6 +875,43 @@ int pg_masked_forward_union(pg_layer L, const uint8_t* masks, size_t P, const in
     PG_API_END
 }
 
+int pg_module_forward_union(const pg_layer* Ls, const uint8_t* const* masks, const size_t* Ps, size_t nlin,
+                            const int32_t* tok_pat, size_t T, const void* x, void* const* ys, pg_dtype ydt,
+                            pg_stream s) {
+    PG_API_BEGIN
+    require(Ls && masks && Ps && tok_pat && x && ys && nlin >= 1 && nlin <= 32 && T > 0, PG_INVALID_ARGUMENT,
+            "module_forward_union: bad arguments");
+    std::vector<size_t> zoff(nlin);
+    size_t zbytes = 0;
+    for (size_t l = 0; l < nlin; ++l) {
+        const pg_layer L = Ls[l];
+        require(L && masks[l] && ys[l] && Ps[l] > 0, PG_INVALID_ARGUMENT, "module_forward_union: bad arguments");
+        require(L->dt == PG_BF16 && L->n == Ls[0]->n && L->n % 8 == 0, PG_INVALID_ARGUMENT,
+                "module_forward_union: bf16 linears sharing one input width (multiple of 8)");
+        check_ydt(L->dt, ydt);
+        zoff[l] = zbytes;
+        zbytes += round_up((size_t)T * round_up((size_t)L->r, 8) * 2, 256);
+    }
+    const cudaStream_t st = as_stream(s);
+    Scratch z(zbytes, st);
+    std::vector<UmmaSpec> s1, s2;
+    for (size_t l = 0; l < nlin; ++l) {
+        const pg_layer L = Ls[l];
+        const int rp = (int)round_up((size_t)L->r, 8);
+        void* zl = z.as<char>() + zoff[l];
+        UmmaSpec a{x, L->n, L->bt, L->ldb, zl, rp, (int)T, rp, L->n, 1};
+        a.mask = masks[l];
+        a.mask_ld = (long long)sel_mask_ld(L->r);
+        a.row_pat = tok_pat;
+        a.b_rows = L->r;
+        s1.push_back(a);
+        s2.push_back(UmmaSpec{zl, rp, L->a, L->lda, ys[l], L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0});
+    }
+    launch_umma(s1, st);  // the linears' first GEMMs share x: one grouped launch
+    launch_umma(s2, st);
+    PG_API_END
+}
+
 // ------------------------------------------------------------ aggregated layout
 int pg_aggregate_layout(pg_agg* out, pg_layer L, const uint32_t* pats, const size_t* ks, size_t P,
                         double psi, pg_stream s) {

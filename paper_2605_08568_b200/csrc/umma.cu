@@ -608,6 +608,33 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
         const int ng = (int)std::min<size_t>(UM_MAX_GROUPS, specs.size() - g0);
         auto P = std::make_unique<UmmaParams>();
         int tiles = 0;
+        // few tiles (small-batch decode through the tensor cores): one narrower
+        // tile width for the whole launch until the SMs are covered, minimising
+        // waves x tile width (time per tile ~ bn x K)
+        int common_bn = 0;
+        {
+            const int rows = pairs ? 2 * UM_BM : UM_BM, slots = pairs ? sms / 2 : sms, step = pairs ? 32 : 16;
+            auto tiles_at = [&](int cap) {
+                long t = 0;
+                for (int g = 0; g < ng; ++g) {
+                    const UmmaSpec& s = specs[g0 + g];
+                    int bn = pick_bn(s.N);
+                    if (pairs) bn = std::min(UM_BN_MAX, (bn + 31) / 32 * 32);
+                    if (cap > 0) bn = std::min(bn, cap);
+                    t += (long)((s.M + rows - 1) / rows) * ((s.N + bn - 1) / bn);
+                }
+                return t;
+            };
+            bool autob = true;
+            for (int g = 0; g < ng; ++g) autob = autob && specs[g0 + g].bn == 0;
+            if (autob && tiles_at(0) < slots) {
+                long best = -1;
+                for (int bn = UM_BN_MAX; bn >= step; bn -= step) {
+                    const long cost = ((tiles_at(bn) + slots - 1) / slots) * (long)bn;
+                    if (best < 0 || cost < best) { best = cost; common_bn = bn; }
+                }
+            }
+        }
         for (int g = 0; g < ng; ++g) {
             const UmmaSpec& s = specs[g0 + g];
             if ((s.lda * 2) % 16 || (s.ldb * 2) % 16 || s.K % 8)
@@ -616,26 +643,8 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             G.bn = pick_bn(s.N);
             if (pairs) G.bn = (G.bn + 31) / 32 * 32;  // each CTA of a pair loads bn/2 rows (multiple of 16)
             if (G.bn > UM_BN_MAX) G.bn = UM_BN_MAX;
-            if (s.bn > 0) {
-                G.bn = s.bn;
-            } else if (ng == 1 && (long)((s.M + (pairs ? 2 * UM_BM : UM_BM) - 1) / (pairs ? 2 * UM_BM : UM_BM)) *
-                                   ((s.N + G.bn - 1) / G.bn) < (pairs ? sms / 2 : sms)) {
-                // a lone GEMM with few tiles (small-batch decode through the
-                // tensor cores): narrower tiles until the SMs are covered,
-                // minimising waves x tile width (time per tile ~ bn x K)
-                const int rows = pairs ? 2 * UM_BM : UM_BM;
-                const int slots = pairs ? sms / 2 : sms;
-                const int tm = (s.M + rows - 1) / rows;
-                const int step = pairs ? 32 : 16;
-                long best = -1;
-                int best_bn = G.bn;
-                for (int bn = G.bn; bn >= step; bn -= step) {
-                    const long tiles_b = (long)tm * ((s.N + bn - 1) / bn);
-                    const long cost = ((tiles_b + slots - 1) / slots) * (long)bn;
-                    if (best < 0 || cost < best) { best = cost; best_bn = bn; }
-                }
-                G.bn = best_bn;
-            }
+            if (s.bn > 0) G.bn = s.bn;
+            else if (common_bn > 0) G.bn = std::min(G.bn, common_bn);
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
             P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
                                           pairs ? G.bn / 2 : G.bn);

@@ -151,3 +151,23 @@ def test_union_masked_batch(pg, port, m, n, r, K, P, T):
     assert rel(one.cpu().numpy(), Y[:1].cpu().numpy()) <= 2e-3
     with pytest.raises(IndexError):
         pg.masked_forward_union(L, batch, [P], X[:1].contiguous())
+
+
+def test_module_forward_union_grouped_equals_single(pg, port):
+    """q/k/v-style linears sharing x through one grouped launch per stage give
+    the single-linear union results bit for bit."""
+    from oracle import pyoracle
+    shapes = [(512, 1024, 384, 192), (256, 1024, 384, 192), (768, 1024, 320, 160)]
+    P, T = 16, 96
+    pats = pyoracle.make_patterns(4242, P, [(r, K) for _, _, r, K in shapes])
+    Ls, Bs = [], []
+    for li, (m, n, r, K) in enumerate(shapes):
+        A, B = layer_data(port, m, n, r, 31 + li)
+        L = pg.FactorizedLayer(A, B, K, dtype="bf16")
+        Ls.append(L)
+        Bs.append(pg.SelectionBatch(L, [pg.RankSelection(p[li]) for p in pats]))
+    pid = np.random.default_rng(3).integers(0, P, T)
+    X = torch.from_numpy(port.gaussian(33, (T, 1024))).cuda().to(torch.bfloat16)
+    ys = pg.module_forward_union(Ls, Bs, pid, X)
+    for L, b, y in zip(Ls, Bs, ys):
+        assert torch.equal(y, pg.masked_forward_union(L, b, pid, X))

@@ -35,6 +35,11 @@ def main():
     ys = {nm: torch.empty(T, m, device=dev, dtype=torch.bfloat16) for nm, (m, n) in SH.items()}
 
     def layer():
+        if os.environ.get("EXP_GROUP", "1") == "1" and not os.environ.get("EXP_ONLY"):
+            for grp in (("q", "k", "v"), ("o",), ("up", "gate"), ("down",)):
+                pg.module_forward_union([lays[g] for g in grp], [batches[g] for g in grp], tp, xs[grp[0]],
+                                        out_dtype=torch.bfloat16, outs=[ys[g] for g in grp])
+            return
         for nm in SH:
             pg.masked_forward_union(lays[nm], batches[nm], tp, xs[nm], out_dtype=torch.bfloat16, out=ys[nm])
 
