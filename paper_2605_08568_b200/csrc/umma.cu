@@ -212,10 +212,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: the next grid may start its prologue now;
+    // this grid reads its operands only after the previous grid completed
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
@@ -444,10 +448,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
     cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_umma_grouped
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             int s = 0;
             uint32_t ph = 0;
             for (int t = pair; t < P.total_tiles; t += npairs) {
@@ -581,6 +587,14 @@ static int pick_bn(int N) {
     return std::min(bn, UM_BN_MAX);
 }
 
+static int umma_pdl() {
+    static const int v = [] {
+        const char* e = getenv("PG_UMMA_PDL");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 static int umma_pairs_enabled() {
     static const int v = [] {
         const char* e = getenv("PG_UMMA_2CTA");
@@ -691,18 +705,30 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             cfg.blockDim = dim3(UM_THREADS);
             cfg.dynamicSmemBytes = U2_SMEM;
             cfg.stream = st;
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = 2;
             at[0].val.clusterDim.y = 1;
             at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[1].val.programmaticStreamSerializationAllowed = umma_pdl();
             cfg.attrs = at;
-            cfg.numAttrs = 1;
+            cfg.numAttrs = 2;
             PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped2, *P));
             count_launch();
         } else {
-            k_umma_grouped<<<std::min(tiles, sms), UM_THREADS, UM_SMEM, st>>>(*P);
-            PG_LAUNCH_CHECK();
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)std::min(tiles, sms));
+            cfg.blockDim = dim3(UM_THREADS);
+            cfg.dynamicSmemBytes = UM_SMEM;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = umma_pdl();
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped, *P));
+            count_launch();
         }
     }
 }
