@@ -239,6 +239,24 @@ int pg_module_forward_union(const pg_layer* layers, const uint8_t* const* masks_
                             size_t n_linears, const int32_t* tok_pat_dev, size_t T, const void* x_dev,
                             void* const* ys_dev, pg_dtype y_dtype, pg_stream stream);
 
+/* Expert-sharded decode (BASELINE config 5) with the all-reduce fused into
+ * the rank-expert kernel: rank `rank` of `npeer` serves its expert shard
+ * (aggregated layout of its experts, `pattern` = the local selection) for one
+ * token; the stage-2 epilogue pushes every output row's partial as a tagged
+ * word into each rank's receive buffer (peer_bufs[r], device pointers of all
+ * ranks' buffers -- NVLink peer memory, opened with pg_ipc_open_handle), and
+ * each CTA then sums its rows over the ranks in rank order, so every rank ends
+ * with the full y (deterministic, identical on all ranks).  Buffers: zeroed
+ * device memory of pg_peer_buffer_bytes(m, npeer) each; all ranks must issue
+ * the same sequence of chain launches on their stream and use the same grid
+ * (0 = all SMs). */
+int pg_peer_buffer_bytes(size_t m, size_t npeer, size_t* bytes);
+int pg_agg_forward_peer(pg_agg shard, size_t pattern, const void* x_dev, void* y_dev, pg_dtype y_dtype, int rank,
+                        int npeer, void* const* peer_bufs, int grid, pg_stream stream);
+int pg_ipc_get_handle(const void* dev_ptr, void* handle64_out);
+int pg_ipc_open_handle(const void* handle64, void** dev_ptr);
+int pg_ipc_close(void* dev_ptr);
+
 /* Heterogeneous prefill (config 3): prompt p owns tokens
  * [offsets_host[p], offsets_host[p+1]) of token-major x (bf16) and its own
  * aggregated layout aggs[p] (served with pattern 0, e.g. the single pattern

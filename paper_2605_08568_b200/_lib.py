@@ -77,6 +77,11 @@ _SIGS = {
     "pg_fill_normal_device": [_vp, _i, _sz, C.c_uint64, C.c_double, _vp],
     "pg_silu_mul": [_vp, _vp, _i, _sz, _vp, _i, _vp],
     "pg_copy_io": [_vp, _vp, _sz, _vp],
+    "pg_peer_buffer_bytes": [_sz, _sz, _vp],
+    "pg_agg_forward_peer": [_vp, _sz, _vp, _vp, _i, _i, _i, _vp, _i, _vp],
+    "pg_ipc_get_handle": [_vp, _vp],
+    "pg_ipc_open_handle": [_vp, _vp],
+    "pg_ipc_close": [_vp],
     "pg_selection_mask_stride": [_vp, _vp],
     "pg_selection_masks": [_vp, _vp, _vp, _sz, _vp, _vp],
     "pg_masked_forward_union": [_vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],

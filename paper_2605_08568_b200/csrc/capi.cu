@@ -609,8 +609,13 @@ static bool chain_ok(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phas
 // Single-launch decode chain (decode.cu).  phases[0] = linears sharing x; when
 // mlp is set, phase 0 is {up, gate} with the silu epilogue into act and phase
 // 1 is {down} reading act.
+struct PeerSpec {  // expert-sharded peer reduction (ChainParams::npeer)
+    int rank = 0, npeer = 0, grid = 0;
+    void* const* bufs = nullptr;
+};
+
 static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, const void* x,
-                      bool mlp, void* act, pg_dtype ydt, cudaStream_t st) {
+                      bool mlp, void* act, pg_dtype ydt, cudaStream_t st, const PeerSpec* peer = nullptr) {
     const size_t accs = wdt == PG_F64 ? 8 : 4, es = dtype_size(wdt);
     ChainParams P = {};
     P.nphase = (int)phases.size();
@@ -664,8 +669,15 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
             off += round_up((size_t)S.cap * zw * 8, 256);
         }
     }
+    int grid = 0;
+    if (peer && peer->npeer > 0) {
+        P.npeer = peer->npeer;
+        P.prank = peer->rank;
+        for (int r = 0; r < peer->npeer; ++r) P.peer_recv[r] = static_cast<unsigned long long*>(peer->bufs[r]);
+        grid = peer->grid;
+    }
     const size_t total = 1024 + xs_bytes + zs_bytes + kRingStages * (128 + 16) + 128 + (size_t)kRingStages * ch;
-    launch_chain(wdt, P, std::min(total, (size_t)227 * 1024), st);
+    launch_chain(wdt, P, std::min(total, (size_t)227 * 1024), st, grid);
 }
 
 // ---- bf16 prefill on the tensor cores (umma.cu): stage 1 and stage 2 of every
@@ -1212,6 +1224,60 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, 
         const LinSpec& D = ph[1][0];
         run_forward(up->dt, D.bt, D.ldb, D.a, D.lda, D.sm, D.cap, D.n, D.m, a, 0, 1, y, ydt, st);
     }
+    PG_API_END
+}
+
+// ------------------------------------------------------------ expert-sharded peer reduction
+int pg_peer_buffer_bytes(size_t m, size_t npeer, size_t* bytes) {
+    PG_API_BEGIN
+    require(bytes && npeer >= 1 && npeer <= (size_t)kMaxPeers && m > 0, PG_INVALID_ARGUMENT,
+            "peer_buffer_bytes: 1..8 ranks");
+    *bytes = 2 * npeer * m * 8;
+    PG_API_END
+}
+
+int pg_agg_forward_peer(pg_agg g, size_t pattern, const void* x, void* y, pg_dtype ydt, int rank, int npeer,
+                        void* const* peer_bufs, int grid, pg_stream s) {
+    PG_API_BEGIN
+    require(g && x && y && peer_bufs && npeer >= 1 && npeer <= kMaxPeers && rank >= 0 && rank < npeer,
+            PG_INVALID_ARGUMENT, "forward_peer: bad arguments");
+    require(g->dt != PG_F64 && ydt != PG_F64, PG_INVALID_ARGUMENT, "forward_peer: bf16/f32 layouts");
+    for (int r = 0; r < npeer; ++r) require(peer_bufs[r] != nullptr, PG_INVALID_ARGUMENT, "forward_peer: null buffer");
+    check_ydt(g->dt, ydt);
+    const std::vector<std::vector<LinSpec>> ph = {{agg_spec(g, (int)pattern, nullptr, y)}};
+    require(chain_ok(g->dt, ph, false), PG_INVALID_ARGUMENT, "forward_peer: layer too wide for the decode chain");
+    PeerSpec ps;
+    ps.rank = rank;
+    ps.npeer = npeer;
+    ps.grid = grid;
+    ps.bufs = peer_bufs;
+    run_chain(g->dt, ph, x, false, nullptr, ydt, as_stream(s), &ps);
+    PG_API_END
+}
+
+int pg_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+    PG_API_BEGIN
+    require(dev_ptr && handle_out, PG_INVALID_ARGUMENT, "ipc: bad arguments");
+    cudaIpcMemHandle_t h;
+    PG_CUDA_THROW(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(handle_out, &h, sizeof(h));
+    PG_API_END
+}
+
+int pg_ipc_open_handle(const void* handle, void** dev_ptr) {
+    PG_API_BEGIN
+    require(handle && dev_ptr, PG_INVALID_ARGUMENT, "ipc: bad arguments");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    PG_CUDA_THROW(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    PG_API_END
+}
+
+int pg_ipc_close(void* dev_ptr) {
+    PG_API_BEGIN
+    require(dev_ptr, PG_INVALID_ARGUMENT, "ipc: null");
+    PG_CUDA_THROW(cudaIpcCloseMemHandle(dev_ptr));
     PG_API_END
 }
 

@@ -12,6 +12,7 @@ constexpr int kMaxLin = 3;
 constexpr int kMaxPhase = 2;
 constexpr int kRingStages = 8;
 constexpr int kMaxChunkItems = 16;
+constexpr int kMaxPeers = 8;
 
 struct ChainLin {
     const void* bt;  // B^T arena [.., ldb] (storage dtype)
@@ -45,9 +46,16 @@ struct ChainParams {
     int chunk_bytes;          // ring stage size
     int max_stages;           // ring depth cap (<= kRingStages)
     unsigned long long* dbg;  // optional per-CTA %globaltimer stamps [grid][16]
+    // expert-sharded peer reduction (single linear, single phase): the stage-2
+    // epilogue pushes each row's partial as a tagged word into every rank's
+    // receive buffer (peer memory over NVLink; [2 parity][npeer][m] words), then
+    // each CTA sums its own rows over the ranks in rank order -- compute and
+    // all-reduce in one kernel, no fence (the tag is in the data word)
+    int npeer, prank;
+    unsigned long long* peer_recv[kMaxPeers];
 };
 
-void launch_chain(pg_dtype wdt, const ChainParams& P, size_t smem, cudaStream_t st);
+void launch_chain(pg_dtype wdt, const ChainParams& P, size_t smem, cudaStream_t st, int grid = 0);
 int chain_grid();
 
 }  // namespace pg

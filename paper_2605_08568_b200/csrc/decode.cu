@@ -516,6 +516,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             for (int e = (nbytes / 16) * 16 / es + tid; e < n; e += nct) xs[e] = static_cast<const W*>(Q.x)[e];
             for (int e = n + tid; e < (n + V - 1) / V * V; e += nct) xs[e] = W(0);
         }
+        if (ph == 0) STAMP(6);  // x staged (thread 0), before the launch tag is needed
         if (ph == 0 && threadIdx.x == 0) *tag_s = (uint32_t)(epoch_old / (unsigned long long)G) + 1u;
         consumer_sync();
         const uint32_t tag = *tag_s;
@@ -693,7 +694,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                             }
                         }
                         acc = warp_sum(acc);
-                        if (lane == 0) {
+                        if (P.npeer) {  // push the partial to every rank (peer memory), reduce below
+                            if (lane < P.npeer) {
+                                const int m = L[l].m;
+                                xput(P.peer_recv[lane] + ((size_t)(tag & 1u) * P.npeer + P.prank) * m + i,
+                                     __float_as_uint((float)acc), tag);
+                            }
+                        } else if (lane == 0) {
                             void* y = L[l].y;
                             if (Q.ydt == PG_F32) static_cast<float*>(y)[i] = (float)acc;
                             else if (Q.ydt == PG_F64) static_cast<double*>(y)[i] = (double)acc;
@@ -710,6 +717,31 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         STAMP(ph * 6 + 5);
         if (ph + 1 < P.nphase) grid_sync_consumers(P.bar);  // act complete before phase ph+1 reads it
     }
+    if (P.npeer) {
+        // this CTA's rows: the npeer partials from this rank's receive buffer,
+        // summed in rank order (deterministic on every rank)
+        const LinS& Lr = lins[(P.nphase - 1) * kMaxLin];
+        const uint32_t tag = *tag_s;
+        const int m = Lr.m;
+        const unsigned long long* mine = P.peer_recv[P.prank] + (size_t)(tag & 1u) * P.npeer * m;
+        for (int i = Lr.i0 + threadIdx.x; i < Lr.i1; i += kConsumerWarps * 32) {
+            unsigned long long w[kMaxPeers];
+#pragma unroll
+            for (int p = 0; p < kMaxPeers; ++p) w[p] = p < P.npeer ? xget(mine + (size_t)p * m + i) : 0ull;
+            float v = 0.f;
+#pragma unroll
+            for (int p = 0; p < kMaxPeers; ++p) {
+                if (p < P.npeer) {
+                    while ((uint32_t)(w[p] >> 32) != tag) w[p] = xget(mine + (size_t)p * m + i);
+                    v += __uint_as_float((uint32_t)w[p]);
+                }
+            }
+            const int ydt = P.ph[P.nphase - 1].ydt;
+            if (ydt == PG_F32) static_cast<float*>(Lr.y)[i] = v;
+            else if (ydt == PG_F64) static_cast<double*>(Lr.y)[i] = (double)v;
+            else static_cast<__nv_bfloat16*>(Lr.y)[i] = __float2bfloat16_rn(v);
+        }
+    }
     STAMP(13);
 }
 
@@ -724,14 +756,14 @@ int chain_grid() {
 }
 
 template <typename W>
-static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st) {
+static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st, int grid) {
     static bool attr = false;
     if (!attr) {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_chain<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(chain_grid());
+    cfg.gridDim = dim3(grid > 0 ? std::min(grid, chain_grid()) : chain_grid());
     cfg.blockDim = dim3(kChainThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -761,10 +793,10 @@ static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st) {
     count_launch();
 }
 
-void launch_chain(pg_dtype wdt, const ChainParams& P, size_t smem, cudaStream_t st) {
-    if (wdt == PG_F64) launch_chain_t<double>(P, smem, st);
-    else if (wdt == PG_F32) launch_chain_t<float>(P, smem, st);
-    else launch_chain_t<__nv_bfloat16>(P, smem, st);
+void launch_chain(pg_dtype wdt, const ChainParams& P, size_t smem, cudaStream_t st, int grid) {
+    if (wdt == PG_F64) launch_chain_t<double>(P, smem, st, grid);
+    else if (wdt == PG_F32) launch_chain_t<float>(P, smem, st, grid);
+    else launch_chain_t<__nv_bfloat16>(P, smem, st, grid);
 }
 
 }  // namespace pg

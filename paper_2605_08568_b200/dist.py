@@ -20,6 +20,7 @@ north star's scale-out of its serving loop (model.hpp:96-106 per prompt).
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -146,3 +147,100 @@ class ShardedLinear:
                                   out_dtype=out_dtype)
 
         return sharded_forward(self.shard, sel, x, fwd, group=self.group)
+
+
+class PeerReduceLinear:
+    """Expert-sharded decode (config 5) with the all-reduce fused into the
+    rank-expert kernel over peer memory (pg_agg_forward_peer): every rank
+    computes its partial A_{S∩E_g}(B_{S∩E_g}^T x) in the decode chain, whose
+    stage-2 epilogue pushes each output row's partial as a tagged word into all
+    ranks' receive buffers (NVLink peer memory); each CTA then sums its rows
+    over the ranks in rank order.  No NCCL call, no fence, and the result is
+    bit-identical on every rank.  T = 1 tokens (decode); prefill chunks go
+    through ShardedLinear.
+
+    Receive buffers are exchanged as CUDA IPC handles over `group` (any
+    torch.distributed backend), or passed in `peer_ptrs` when the ranks live in
+    one process (tests: virtual ranks on one GPU, each on its own stream with a
+    grid small enough that all ranks' kernels are co-resident)."""
+
+    def __init__(self, A, B, world: int, rank: int, dtype="bf16", group=None, grid: int = 0, psi: float = 0.9):
+        from .api import FactorizedLayer, call
+        if not 1 <= world <= 8:
+            raise ValueError("PeerReduceLinear: 1..8 ranks")
+        self.shard = shard_layer(np.asarray(A, dtype=np.float64), np.asarray(B, dtype=np.float64), world, rank)
+        self.world, self.rank, self.grid, self.psi = world, rank, grid, psi
+        self.m, self.n = self.shard.A.shape[0], self.shard.B.shape[0]
+        self.local = FactorizedLayer(self.shard.A, self.shard.B, None, dtype=dtype)
+        nb = C.c_size_t()
+        call("pg_peer_buffer_bytes", self.m, world, C.byref(nb))
+        self.recv = torch.zeros(nb.value // 8, dtype=torch.int64, device="cuda")  # tags start at 1: zero = empty
+        self.peer_ptrs = None
+        self._opened = []
+        self._aggs = {}
+        self._last = None
+        if group is not None and world > 1:
+            self._exchange(group)
+
+    def _exchange(self, group):
+        import torch.distributed as dist
+        from .api import call
+        h = (C.c_char * 64)()
+        call("pg_ipc_get_handle", C.c_void_p(self.recv.data_ptr()), h)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        ptrs = []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(self.recv.data_ptr())
+                continue
+            p = C.c_void_p()
+            call("pg_ipc_open_handle", (C.c_char * 64).from_buffer_copy(hb), C.byref(p))
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self.peer_ptrs = ptrs
+
+    @staticmethod
+    def local_group(A, B, world: int, dtype="bf16", grid: int = 0) -> list:
+        """All ranks in this process (virtual ranks sharing one device)."""
+        ranks = [PeerReduceLinear(A, B, world, r, dtype=dtype, grid=grid) for r in range(world)]
+        ptrs = [r.recv.data_ptr() for r in ranks]
+        for r in ranks:
+            r.peer_ptrs = ptrs
+        return ranks
+
+    def prepare(self, sel):
+        """Pack this rank's share of the selection (reused across decode steps)."""
+        from .api import RankSelection, aggregate_layout
+        if self._last is not None and self._last[0] is sel:  # decode steps reuse the same selection object
+            return self._last[1]
+        key = tuple(int(v) for v in np.asarray(sel.indices if hasattr(sel, "indices") else sel))
+        if key not in self._aggs:
+            mine = shard_selection(np.asarray(key, dtype=np.int64), self.world, self.rank)
+            if mine.size == 0:
+                raise ValueError("PeerReduceLinear: this rank owns none of the selected experts")
+            self._aggs[key] = aggregate_layout(self.local, [RankSelection(self.shard.local_ids(mine))], self.psi)
+        self._last = (sel, self._aggs[key])
+        return self._aggs[key]
+
+    def forward(self, sel, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None) -> torch.Tensor:
+        from .api import _TORCH, _dtype_code, _ptr, call
+        if self.peer_ptrs is None:
+            raise RuntimeError("PeerReduceLinear: receive buffers not exchanged")
+        agg = self.prepare(sel)
+        x = x.reshape(-1)
+        if x.numel() != self.n:
+            raise ValueError("PeerReduceLinear: one token (x of n elements)")
+        x = x.to(self.local.torch_dtype).contiguous()
+        ydt = _dtype_code(out_dtype)
+        y = out if out is not None else torch.empty(self.m, dtype=_TORCH[ydt], device=x.device)
+        ptrs = (C.c_void_p * self.world)(*self.peer_ptrs)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        call("pg_agg_forward_peer", agg.handle, 0, _ptr(x), _ptr(y), ydt, self.rank, self.world, ptrs, self.grid, st)
+        return y
+
+    def close(self):
+        from .api import call
+        for p in self._opened:
+            call("pg_ipc_close", p)
+        self._opened = []

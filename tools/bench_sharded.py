@@ -58,14 +58,36 @@ def main():
     torch.cuda.synchronize()
     ms = pgd.max_over_ranks(e0.elapsed_time(e1) / reps, device=torch.device("cuda"))
     y = lin.forward(sel, xd).double().cpu().numpy()
+    full = pg.FactorizedLayer(A, B, K, dtype="bf16")
+    yr = pg.masked_forward(full, sel, xd, out_dtype=torch.float32).double().cpu().numpy()
     if rank == 0:
-        full = pg.FactorizedLayer(A, B, K, dtype="bf16")
-        yr = pg.masked_forward(full, sel, xd, out_dtype=torch.float32).double().cpu().numpy()
         rel = float(np.abs(y - yr).max() / np.abs(yr).max())
         print(json.dumps({"workload": "config5 shapes: 13824x5120 ratio 0.4 expert-sharded (e mod G)",
                           "world": world, "ms_per_step": ms, "step": "1 x T=256 prefill + 8 x T=1 decode",
                           "tokens_per_s": (256 + 8) / (ms * 1e-3), "rel_vs_single_gpu": rel,
                           "per_rank_weight_bytes": int((lin.shard.A.shape[1]) * (m + n) * 2)}))
+    # decode steps with the all-reduce fused into the kernel over peer memory
+    if world > 1:
+        fused = pgd.PeerReduceLinear(A, B, world, rank, dtype="bf16", group=dist.group.WORLD)
+    else:
+        fused = pgd.PeerReduceLinear.local_group(A, B, 1, dtype="bf16")[0]
+    fused.prepare(sel)
+    for _ in range(3):
+        fused.forward(sel, xd)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record()
+    for _ in range(reps * 8):
+        fused.forward(sel, xd)
+    e1.record()
+    torch.cuda.synchronize()
+    fus_us = pgd.max_over_ranks(e0.elapsed_time(e1) / (reps * 8) * 1e3, device=torch.device("cuda"))
+    yf = fused.forward(sel, xd).double().cpu().numpy()
+    if rank == 0:
+        relf = float(np.abs(yf - yr[:, 0]).max() / np.abs(yr).max())
+        print(json.dumps({"fused_peer_decode_us_per_token": fus_us, "rel_vs_single_gpu": relf}))
+    fused.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -75,10 +75,9 @@ def stamps():
     _lib.call("pg_chain_debug_dump", buf, 1024 * 16)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16)[:148].astype(np.int64)
     t0 = a[:, 0].min()
-    names = ["start", "x0", "s1done0", "bar0", "z0", "s2done0", "x1", "s1done1", "bar1", "z1", "s2done1", "prod_done", "end"]
+    names = ["start", "x0", "s1done0", "bar0", "z0", "s2done0", "xstaged0", "x1", "s1done1", "bar1", "z1", "s2done1",
+             "prod_done", "end"]
     for k, nm in enumerate(names):
-        if k >= 6:
-            k += 1
         col = a[:, k]
         if (col > 0).all():
             print(f"{nm:9s} min {(col.min() - t0) / 1e3:7.2f} med {(np.median(col) - t0) / 1e3:7.2f} "
