@@ -423,7 +423,7 @@ __device__ void chain_producer(const ChainParams& P, const LinS* lins, Desc* des
 }
 
 // ---------------------------------------------------------------- kernel
-template <typename W>
+template <typename W, bool PEER>
 __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constant__ ChainParams P) {
     using A = typename Acc<W>::type;
     constexpr int V = CVec<W>::n;
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                             }
                         }
                         acc = warp_sum(acc);
-                        if (P.npeer) {  // push the partial to every rank (peer memory), reduce below
+                        if constexpr (PEER) {  // push the partial to every rank (peer memory), reduce below
                             if (lane < P.npeer) {
                                 const int m = L[l].m;
                                 xput(P.peer_recv[lane] + ((size_t)(tag & 1u) * P.npeer + P.prank) * m + i,
@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         STAMP(ph * 6 + 5);
         if (ph + 1 < P.nphase) grid_sync_consumers(P.bar);  // act complete before phase ph+1 reads it
     }
-    if (P.npeer) {
+    if constexpr (PEER) {
         // this CTA's rows: the npeer partials from this rank's receive buffer,
         // summed in rank order (deterministic on every rank)
         const LinS& Lr = lins[(P.nphase - 1) * kMaxLin];
@@ -755,11 +755,11 @@ int chain_grid() {
     return g_num_sms;
 }
 
-template <typename W>
+template <typename W, bool PEER>
 static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st, int grid) {
     static bool attr = false;
     if (!attr) {
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_chain<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_chain<W, PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -789,14 +789,22 @@ static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st, i
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_chain<W>, P));
+    PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_chain<W, PEER>, P));
     count_launch();
 }
 
 void launch_chain(pg_dtype wdt, const ChainParams& P, size_t smem, cudaStream_t st, int grid) {
-    if (wdt == PG_F64) launch_chain_t<double>(P, smem, st, grid);
-    else if (wdt == PG_F32) launch_chain_t<float>(P, smem, st, grid);
-    else launch_chain_t<__nv_bfloat16>(P, smem, st, grid);
+    // the peer-reduction variant is a separate instantiation so the hot MLP
+    // kernel keeps its register budget
+    if (P.npeer) {
+        if (wdt == PG_F32) launch_chain_t<float, true>(P, smem, st, grid);
+        else if (wdt == PG_BF16) launch_chain_t<__nv_bfloat16, true>(P, smem, st, grid);
+        else throw Error{PG_INVALID_ARGUMENT, "decode chain: peer reduction needs bf16/f32"};
+        return;
+    }
+    if (wdt == PG_F64) launch_chain_t<double, false>(P, smem, st, grid);
+    else if (wdt == PG_F32) launch_chain_t<float, false>(P, smem, st, grid);
+    else launch_chain_t<__nv_bfloat16, false>(P, smem, st, grid);
 }
 
 }  // namespace pg
