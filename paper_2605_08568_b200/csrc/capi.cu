@@ -597,7 +597,11 @@ static size_t chain_chunk_bytes(pg_dtype wdt, const std::vector<std::vector<LinS
     const size_t fixed = 1024 + xs + zs + kRingStages * (128 + 16) + 128;
     const size_t kMaxSmem = 227 * 1024;
     if (fixed + 2 * item > kMaxSmem) return 0;  // need >= 2 stages in flight
-    size_t ch = (kMaxSmem - fixed) / kRingStages / 128 * 128;
+    static const int div_env = [] {  // experiments: size chunks for this many stages
+        const char* e = getenv("PG_CHAIN_CHUNK_DIV");
+        return e ? std::max(2, std::min(atoi(e), kRingStages)) : kRingStages;
+    }();
+    size_t ch = (kMaxSmem - fixed) / div_env / 128 * 128;
     return std::max(ch, round_up(item, 128));
 }
 
