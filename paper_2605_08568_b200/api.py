@@ -871,13 +871,21 @@ def mlp_forward(up: "AggregatedLayer", gate: "AggregatedLayer", down: "Aggregate
                 x: torch.Tensor, out_dtype=None, out: torch.Tensor | None = None,
                 act: torch.Tensor | None = None) -> torch.Tensor:
     """One decode token (T=1) through a rank-expert MLP block in ONE kernel:
-    up/gate share x, act = silu(gate)*up (toy_lm.hpp:250-257), y = down(act)."""
-    x = _dev(x, up.layer.torch_dtype).reshape(-1)
+    up/gate share x, act = silu(gate)*up (toy_lm.hpp:250-257), y = down(act).
+    x and out may be pinned host tensors: the kernel then reads the token and
+    writes the result over the host link itself (zero-copy step I/O)."""
+    def io_ptr(t):
+        if t.is_pinned() and t.is_contiguous():
+            return t.data_ptr()
+        return _ptr(t)
+    if not (isinstance(x, torch.Tensor) and x.is_pinned() and x.dtype == up.layer.torch_dtype):
+        x = _dev(x, up.layer.torch_dtype)
+    x = x.reshape(-1)
     ydt = _out_dtype(up.layer.dtype, out_dtype)
-    y = out if out is not None else torch.empty(down.m, dtype=_TORCH[ydt], device=x.device)
+    y = out if out is not None else torch.empty(down.m, dtype=_TORCH[ydt], device="cuda")
     parr, pdev = _pattern_args(pattern_ids, 3)
-    call("pg_mlp_forward", up.handle, gate.handle, down.handle, parr, pdev, _ptr(x),
-         _ptr(act) if act is not None else None, _ptr(y), ydt, _stream())
+    call("pg_mlp_forward", up.handle, gate.handle, down.handle, parr, pdev, io_ptr(x),
+         _ptr(act) if act is not None else None, io_ptr(y), ydt, _stream())
     return y
 
 

@@ -568,6 +568,12 @@ def test_mlp_forward_single_kernel_matches_oracle(pg, port, dtype):
         pdev = torch.tensor([pid], dtype=torch.int32, device="cuda")
         y3 = pg.mlp_forward(aggs["up"], aggs["gate"], aggs["down"], pdev, xd)
         assert torch.equal(y, y3)
+        # zero-copy step I/O: x read from / y written to pinned host memory by the kernel
+        xh = xd.cpu().pin_memory()
+        yh = torch.zeros(d, dtype=y.dtype).pin_memory()
+        pg.mlp_forward(aggs["up"], aggs["gate"], aggs["down"], pid, xh, out=yh)
+        torch.cuda.synchronize()
+        assert torch.equal(yh, y.cpu())
 
 
 def test_module_forward_qkv_gqa(pg, port):
