@@ -637,6 +637,14 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
         return e ? std::max(2, std::min(atoi(e), kRingStages)) : 0;
     }();
     P.max_stages = stages_env ? stages_env : (mlp ? kRingStages - 1 : kRingStages);
+    // producer throttle across the z exchange: after a stage-1 segment at most 3
+    // chunks are issued until the consumers have the exchanged z (less HBM
+    // traffic queued ahead of the exchange); measured -2 % per MLP step
+    static const int throttle_env = [] {
+        const char* e = getenv("PG_CHAIN_THROTTLE");
+        return e ? atoi(e) : -2;
+    }();
+    P.throttle = throttle_env != -2 ? throttle_env : (mlp ? 3 : -1);
     P.dbg = chain_debug_buffer();
     const size_t zw = wdt == PG_F64 ? 2 : 1;  // tagged exchange words per z value
     size_t zbytes = 256;

@@ -51,6 +51,7 @@ struct ChainParams {
     // receive buffer (peer memory over NVLink; [2 parity][npeer][m] words), then
     // each CTA sums its own rows over the ranks in rank order -- compute and
     // all-reduce in one kernel, no fence (the tag is in the data word)
+    int throttle;  // >= 0: after a stage-1 segment, at most this many chunks until the z exchange is done
     int npeer, prank;
     unsigned long long* peer_recv[kMaxPeers];
 };

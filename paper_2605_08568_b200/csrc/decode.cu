@@ -311,12 +311,22 @@ __device__ void chain_producer(const ChainParams& P, const LinS* lins, Desc* des
     constexpr int es = sizeof(W);
     const int CH = P.chunk_bytes;
     int k = 0;
+    int throttle_left = -1;  // chunks still allowed before the z exchange completes (-1: unlimited)
+    int zphase = 0;
+    uint64_t* zbar = empty + kRingStages + 1;
     unsigned uses = 0;      // parity of the next empty-wait per stage (bit k)
     unsigned used_once = 0;
     int gidx = 0;
     int c_used = 0, c_cnt = 0;
     Desc* d = nullptr;
     auto open = [&](int seg, int lin) {
+        if (throttle_left == 0) {  // hold the stream until the consumers finished the z exchange
+            mbar_wait(smem_u32(zbar), (uint32_t)(zphase & 1));
+            ++zphase;
+            throttle_left = -1;
+        } else if (throttle_left > 0) {
+            --throttle_left;
+        }
         if (used_once & (1u << k)) {
             mbar_wait(smem_u32(&empty[k]), (uses >> k) & 1u);
             uses ^= 1u << k;
@@ -347,6 +357,11 @@ __device__ void chain_producer(const ChainParams& P, const LinS* lins, Desc* des
     for (int ph = 0; ph < P.nphase; ++ph) {
         const ChainPhase& Q = P.ph[ph];
         const LinS* L = lins + ph * kMaxLin;
+        if (P.throttle >= 0 && zphase < ph) {  // absorb the previous phase's exchange signal
+            mbar_wait(smem_u32(zbar), (uint32_t)(zphase & 1));
+            ++zphase;
+            throttle_left = -1;
+        }
         // ---- stage-1 segment: B^T rows of this CTA's slot range.  Slots of one
         // run are consecutive B^T rows, so a chunk is ONE bulk copy; masked slots
         // ride along and are zeroed when z is staged.
@@ -368,6 +383,7 @@ __device__ void chain_producer(const ChainParams& P, const LinS* lins, Desc* des
         }
         open(2 * ph, 0);
         close(1);
+        if (P.throttle >= 0) throttle_left = P.throttle;
         // ---- stage-2 segment: A_S rows of this CTA's row range.  Single-run
         // arenas (lda == nslots) are contiguous: one copy per matrix per chunk.
         if (Q.epilogue == 1) {
@@ -475,6 +491,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             mbar_init(smem_u32(&full[k]), 1);
             mbar_init(smem_u32(&empty[k]), kConsumerWarps);
         }
+        mbar_init(smem_u32(empty + kRingStages + 1), 1);  // z exchange done (producer throttle)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -618,6 +635,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         }
         consumer_sync();
         STAMP(ph * 6 + 4);
+        if (P.throttle >= 0 && threadIdx.x == 0) mbar_arrive(smem_u32(empty + kRingStages + 1));
         // bf16 with <= 2 linears of <= 32 * 8 * kRowJ slots: z into registers
         ZReg zr0, zr1;
         bool zreg = false;
