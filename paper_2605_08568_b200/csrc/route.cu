@@ -221,6 +221,85 @@ k_score_fast(const double* __restrict__ theta, const double* __restrict__ bias, 
     }
 }
 
+// Same as k_score_fast with two 8-row theta tiles per block and 16 k-slices:
+// every h fragment load feeds both tiles (half the L2 traffic for h, which
+// all blocks re-read), same occupancy.  Partial tiles summed in fixed slice
+// order; the error bound argument is unchanged.
+constexpr int kScoreSlices2 = 16;
+__global__ void __launch_bounds__(kScoreSlices2 * 32)
+k_score_fast2(const double* __restrict__ theta, const double* __restrict__ bias, int r, int n,
+              const double* __restrict__ h, const double* __restrict__ hnorm, int P, double* __restrict__ z,
+              double* __restrict__ bnd) {
+    __shared__ double part[kScoreSlices2][32][10];  // per lane: 2 row tiles x (2 prompt tiles x 2) + 2 row-norm partials
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row0 = blockIdx.x * 16, p0 = blockIdx.y * 16;
+    const int rr = lane >> 2, cc = lane & 3;
+    const double* th0 = theta + (int64_t)min(row0 + rr, r - 1) * n;
+    const double* th1 = theta + (int64_t)min(row0 + 8 + rr, r - 1) * n;
+    const double* h0 = h + (int64_t)min(p0 + rr, P - 1) * n;
+    const double* h1 = h + (int64_t)min(p0 + 8 + rr, P - 1) * n;
+    const int ng = (n + 7) / 8;
+    const int g0 = (int)((long long)ng * warp / kScoreSlices2), g1 = (int)((long long)ng * (warp + 1) / kScoreSlices2);
+    double d[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    double nrm0 = 0.0, nrm1 = 0.0;
+    const bool vec = (n & 1) == 0;
+#pragma unroll 2
+    for (int gi = g0; gi < g1; ++gi) {
+        const int k = gi * 8 + 2 * cc;
+        double2 t0, t1, a, b;
+        if (vec && k + 1 < n) {
+            t0 = __ldg(reinterpret_cast<const double2*>(th0 + k));
+            t1 = __ldg(reinterpret_cast<const double2*>(th1 + k));
+            a = __ldg(reinterpret_cast<const double2*>(h0 + k));
+            b = __ldg(reinterpret_cast<const double2*>(h1 + k));
+        } else {
+            t0.x = k < n ? th0[k] : 0.0;  t0.y = k + 1 < n ? th0[k + 1] : 0.0;
+            t1.x = k < n ? th1[k] : 0.0;  t1.y = k + 1 < n ? th1[k + 1] : 0.0;
+            a.x = k < n ? h0[k] : 0.0;   a.y = k + 1 < n ? h0[k + 1] : 0.0;
+            b.x = k < n ? h1[k] : 0.0;   b.y = k + 1 < n ? h1[k + 1] : 0.0;
+        }
+        nrm0 = fma(t0.y, t0.y, fma(t0.x, t0.x, nrm0));
+        nrm1 = fma(t1.y, t1.y, fma(t1.x, t1.x, nrm1));
+        dmma(d[0][0], d[0][1], t0.x, a.x);
+        dmma(d[0][2], d[0][3], t0.x, b.x);
+        dmma(d[1][0], d[1][1], t1.x, a.x);
+        dmma(d[1][2], d[1][3], t1.x, b.x);
+        dmma(d[0][0], d[0][1], t0.y, a.y);
+        dmma(d[0][2], d[0][3], t0.y, b.y);
+        dmma(d[1][0], d[1][1], t1.y, a.y);
+        dmma(d[1][2], d[1][3], t1.y, b.y);
+    }
+    nrm0 += __shfl_xor_sync(0xffffffffu, nrm0, 1);
+    nrm0 += __shfl_xor_sync(0xffffffffu, nrm0, 2);
+    nrm1 += __shfl_xor_sync(0xffffffffu, nrm1, 1);
+    nrm1 += __shfl_xor_sync(0xffffffffu, nrm1, 2);
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) part[warp][lane][t * 4 + e] = d[t][e];
+    part[warp][lane][8] = nrm0;
+    part[warp][lane][9] = nrm1;
+    __syncthreads();
+    if (threadIdx.x < 256) {  // (row i, prompt q) = (t / 16, t % 16), rows of both tiles
+        const int i = threadIdx.x >> 4, q = threadIdx.x & 15;
+        const int tile = i >> 3, ii = i & 7;
+        const int L = ii * 4 + ((q & 7) >> 1), e = (q >= 8 ? 2 : 0) + (q & 1);
+        double acc = 0.0, nr = 0.0;
+        for (int w = 0; w < kScoreSlices2; ++w) {
+            acc += part[w][L][tile * 4 + e];
+            nr += part[w][ii * 4][8 + tile];
+        }
+        const int R = row0 + i, p = p0 + q;
+        if (R < r && p < P) {
+            const double gam = 4.0 * (double)(n + 2) * kU;
+            const double tiny = 4.0 * (double)(n + 2) * 4.9406564584124654e-324;
+            const double b = bias[R];
+            z[(int64_t)p * r + R] = acc + b;
+            if (bnd) bnd[(int64_t)p * r + R] = gam * (sqrt(nr) * hnorm[p] + fabs(b)) * 1.0000001 + tiny;
+        }
+    }
+}
+
 // reference order: dot (matrix.hpp:189-193) then + bias; one lane per row,
 // theta tiles staged through shared memory so global reads stay coalesced.
 __device__ __forceinline__ double ref_dot_row(const double* __restrict__ th,
@@ -411,8 +490,17 @@ void launch_score(const double* theta, const double* bias, int r, int n, const d
         // hnorm: caller scratch of P doubles
         k_hnorm<<<P, 256, 0, st>>>(h, n, hnorm);
         PG_LAUNCH_CHECK();
-        dim3 g((r + 7) / 8, (P + 15) / 16);
-        k_score_fast<<<g, kScoreSlices * 32, 0, st>>>(theta, bias, r, n, h, hnorm, P, z, bnd);
+        static const int v2 = [] {
+            const char* e = getenv("PG_SCORE_V2");
+            return e ? atoi(e) : 1;
+        }();
+        if (v2) {
+            dim3 g((r + 15) / 16, (P + 15) / 16);
+            k_score_fast2<<<g, kScoreSlices2 * 32, 0, st>>>(theta, bias, r, n, h, hnorm, P, z, bnd);
+        } else {
+            dim3 g((r + 7) / 8, (P + 15) / 16);
+            k_score_fast<<<g, kScoreSlices * 32, 0, st>>>(theta, bias, r, n, h, hnorm, P, z, bnd);
+        }
     }
     PG_LAUNCH_CHECK();
 }
