@@ -162,6 +162,28 @@ def test_mean_pool_bf16_token_major_batched(pg, port):
         assert np.array_equal(h[p], port.mean_pool(Xr[offs[p]:offs[p + 1]].T)), p
 
 
+def test_mean_pool_long_prompts_adversarial_columns(pg, port):
+    """Long prompts with adversarial columns (tiny and huge values in one
+    feature, a bf16-subnormal-range value, Inf, exact cancellation) pool to the
+    reference's sequential sum bit for bit."""
+    n = 512
+    lens = [2048, 1500, 777]
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    X = port.gaussian(96, (offs[-1], n))
+    X[offs[1] + 3, 5] = 1e-30      # spread too wide for an exact split: fallback
+    X[offs[1] + 900, 5] = 3e4
+    X[offs[2] + 10, 9] = 1e-38     # bf16 subnormal-range value
+    X[offs[0] + 7, 11] = np.inf    # non-finite: fallback keeps the reference's result
+    X[offs[0]:offs[1], 13] = 0.0
+    X[offs[0] + 5, 13], X[offs[0] + 1999, 13] = 2.5, -2.5  # exact cancellation
+    Xb = torch.from_numpy(X).cuda().to(torch.bfloat16)
+    Xr = Xb.double().cpu().numpy()
+    h = pg.mean_pool(Xb, layout="token", offsets=offs).cpu().numpy()
+    for p in range(len(lens)):
+        ref = port.mean_pool(Xr[offs[p]:offs[p + 1]].T)
+        assert np.array_equal(h[p], ref, equal_nan=True), p
+
+
 @pytest.mark.parametrize("nbytes", [1, 15, 16, 8192, 16384 + 7])
 def test_copy_io_pinned_roundtrip(pg, nbytes):
     src = torch.randint(0, 255, (nbytes,), dtype=torch.uint8).pin_memory()
