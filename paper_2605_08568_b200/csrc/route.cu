@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kScoreSlices2 * 32)
 k_score_fast2(const double* __restrict__ theta, const double* __restrict__ bias, int r, int n,
               const double* __restrict__ h, const double* __restrict__ hnorm, int P, double* __restrict__ z,
               double* __restrict__ bnd) {
-    __shared__ double part[kScoreSlices2][32][10];  // per lane: 2 row tiles x (2 prompt tiles x 2) + 2 row-norm partials
+    __shared__ double part[kScoreSlices2][32][12];  // per lane: 2 row tiles x (2 prompt tiles x 2) + 2 row-norm + 2 h-norm partials
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row0 = blockIdx.x * 16, p0 = blockIdx.y * 16;
     const int rr = lane >> 2, cc = lane & 3;
@@ -241,7 +241,7 @@ k_score_fast2(const double* __restrict__ theta, const double* __restrict__ bias,
     const int ng = (n + 7) / 8;
     const int g0 = (int)((long long)ng * warp / kScoreSlices2), g1 = (int)((long long)ng * (warp + 1) / kScoreSlices2);
     double d[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-    double nrm0 = 0.0, nrm1 = 0.0;
+    double nrm0 = 0.0, nrm1 = 0.0, hn0 = 0.0, hn1 = 0.0;
     const bool vec = (n & 1) == 0;
 #pragma unroll 2
     for (int gi = g0; gi < g1; ++gi) {
@@ -260,6 +260,8 @@ k_score_fast2(const double* __restrict__ theta, const double* __restrict__ bias,
         }
         nrm0 = fma(t0.y, t0.y, fma(t0.x, t0.x, nrm0));
         nrm1 = fma(t1.y, t1.y, fma(t1.x, t1.x, nrm1));
+        hn0 = fma(a.y, a.y, fma(a.x, a.x, hn0));  // ||h|| of the block's prompts, fused (no k_hnorm pass)
+        hn1 = fma(b.y, b.y, fma(b.x, b.x, hn1));
         dmma(d[0][0], d[0][1], t0.x, a.x);
         dmma(d[0][2], d[0][3], t0.x, b.x);
         dmma(d[1][0], d[1][1], t1.x, a.x);
@@ -273,21 +275,28 @@ k_score_fast2(const double* __restrict__ theta, const double* __restrict__ bias,
     nrm0 += __shfl_xor_sync(0xffffffffu, nrm0, 2);
     nrm1 += __shfl_xor_sync(0xffffffffu, nrm1, 1);
     nrm1 += __shfl_xor_sync(0xffffffffu, nrm1, 2);
+    hn0 += __shfl_xor_sync(0xffffffffu, hn0, 1);
+    hn0 += __shfl_xor_sync(0xffffffffu, hn0, 2);
+    hn1 += __shfl_xor_sync(0xffffffffu, hn1, 1);
+    hn1 += __shfl_xor_sync(0xffffffffu, hn1, 2);
 #pragma unroll
     for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int e = 0; e < 4; ++e) part[warp][lane][t * 4 + e] = d[t][e];
     part[warp][lane][8] = nrm0;
     part[warp][lane][9] = nrm1;
+    part[warp][lane][10] = hn0;
+    part[warp][lane][11] = hn1;
     __syncthreads();
     if (threadIdx.x < 256) {  // (row i, prompt q) = (t / 16, t % 16), rows of both tiles
         const int i = threadIdx.x >> 4, q = threadIdx.x & 15;
         const int tile = i >> 3, ii = i & 7;
         const int L = ii * 4 + ((q & 7) >> 1), e = (q >= 8 ? 2 : 0) + (q & 1);
-        double acc = 0.0, nr = 0.0;
+        double acc = 0.0, nr = 0.0, hn = 0.0;
         for (int w = 0; w < kScoreSlices2; ++w) {
             acc += part[w][L][tile * 4 + e];
             nr += part[w][ii * 4][8 + tile];
+            hn += part[w][(q & 7) * 4][10 + (q >> 3)];
         }
         const int R = row0 + i, p = p0 + q;
         if (R < r && p < P) {
@@ -295,7 +304,8 @@ k_score_fast2(const double* __restrict__ theta, const double* __restrict__ bias,
             const double tiny = 4.0 * (double)(n + 2) * 4.9406564584124654e-324;
             const double b = bias[R];
             z[(int64_t)p * r + R] = acc + b;
-            if (bnd) bnd[(int64_t)p * r + R] = gam * (sqrt(nr) * hnorm[p] + fabs(b)) * 1.0000001 + tiny;
+            // norms carry O(n u) relative rounding, far inside the 1e-7 inflation
+            if (bnd) bnd[(int64_t)p * r + R] = gam * (sqrt(nr) * sqrt(hn) + fabs(b)) * 1.0000001 + tiny;
         }
     }
 }
@@ -487,13 +497,14 @@ void launch_score(const double* theta, const double* bias, int r, int n, const d
         dim3 g((r + 127) / 128, P);
         k_score_exact<<<g, 128, 0, st>>>(theta, bias, r, n, h, P, z);
     } else {
-        // hnorm: caller scratch of P doubles
-        k_hnorm<<<P, 256, 0, st>>>(h, n, hnorm);
-        PG_LAUNCH_CHECK();
         static const int v2 = [] {
             const char* e = getenv("PG_SCORE_V2");
             return e ? atoi(e) : 1;
         }();
+        if (!v2) {  // hnorm: caller scratch of P doubles (v2 fuses the norm)
+            k_hnorm<<<P, 256, 0, st>>>(h, n, hnorm);
+            PG_LAUNCH_CHECK();
+        }
         if (v2) {
             dim3 g((r + 15) / 16, (P + 15) / 16);
             k_score_fast2<<<g, kScoreSlices2 * 32, 0, st>>>(theta, bias, r, n, h, hnorm, P, z, bnd);
