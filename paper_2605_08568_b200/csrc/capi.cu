@@ -684,7 +684,11 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
             off += round_up((size_t)S.cap * zw * 8, 256);
         }
     }
-    int grid = 0;
+    static const int grid_env = [] {  // experiments: decode-chain grid size (default: every SM)
+        const char* e = getenv("PG_CHAIN_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    int grid = grid_env;
     if (peer && peer->npeer > 0) {
         P.npeer = peer->npeer;
         P.prank = peer->rank;
