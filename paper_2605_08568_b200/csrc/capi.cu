@@ -901,8 +901,11 @@ int pg_masked_forward_union(pg_layer L, const uint8_t* masks, size_t P, const in
     s1.mask_ld = (long long)sel_mask_ld(L->r);
     s1.row_pat = tok_pat;
     s1.b_rows = L->r;
-    launch_umma({s1}, st);
-    launch_umma({UmmaSpec{z.p, rp, L->a, L->lda, y, L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0}}, st);
+    const UmmaSpec s2{z.p, rp, L->a, L->lda, y, L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0};
+    // long K with few tiles: split K across the SMs (f32 partials), else narrow tiles
+    Scratch ws(std::max(umma_splitk_bytes(s1), umma_splitk_bytes(s2)), st);
+    if (!launch_umma_splitk(s1, ws.p, st)) launch_umma({s1}, st);
+    if (!launch_umma_splitk(s2, ws.p, st)) launch_umma({s2}, st);
     PG_API_END
 }
 
@@ -938,8 +941,14 @@ int pg_module_forward_union(const pg_layer* Ls, const uint8_t* const* masks, con
         s1.push_back(a);
         s2.push_back(UmmaSpec{zl, rp, L->a, L->lda, ys[l], L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0});
     }
-    launch_umma(s1, st);  // the linears' first GEMMs share x: one grouped launch
-    launch_umma(s2, st);
+    // the linears' first GEMMs share x: one grouped launch per stage (with
+    // their K split across the SMs when that pays, see launch_umma_splitk)
+    size_t w1 = 0, w2 = 0;
+    for (const UmmaSpec& u : s1) w1 += umma_splitk_bytes(u);
+    for (const UmmaSpec& u : s2) w2 += umma_splitk_bytes(u);
+    Scratch ws(std::max(w1, w2), st);
+    if (!launch_umma_splitk_multi(s1, ws.p, st)) launch_umma(s1, st);
+    if (!launch_umma_splitk_multi(s2, ws.p, st)) launch_umma(s2, st);
     PG_API_END
 }
 

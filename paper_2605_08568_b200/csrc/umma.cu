@@ -47,6 +47,7 @@ struct UmmaGroup {
     const uint8_t* mask;       // nullable: per-row column mask (see UmmaSpec)
     long long mask_ld;
     const int32_t* row_pat;
+    int direct_epi;
 };
 
 // Passed as one __grid_constant__ parameter block (< 32 KB): TMA reads the
@@ -521,7 +522,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
-            epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf);
+            if (G.direct_epi) epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
+            else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
@@ -662,6 +664,7 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
             P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
                                           pairs ? G.bn / 2 : G.bn);
+            G.direct_epi = s.direct_epi;
             G.mask = s.mask;
             G.mask_ld = s.mask_ld;
             G.row_pat = s.row_pat;
@@ -731,6 +734,128 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             count_launch();
         }
     }
+}
+
+// ---------------------------------------------------------------- split-K
+__global__ void k_splitk_reduce(const float* __restrict__ part, int S, int M, int N, const uint8_t* __restrict__ mask,
+                                long long mask_ld, const int32_t* __restrict__ row_pat, void* out, long long ldo,
+                                int out_bf16) {
+    const long long slice = (long long)M * N, n4 = slice / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        const long long e = 4 * i;
+        const int row = (int)(e / N), col = (int)(e % N);
+        float4 a = __ldcs(reinterpret_cast<const float4*>(part + e));
+        for (int q = 1; q < S; ++q) {  // slice order: deterministic
+            const float4 b = __ldcs(reinterpret_cast<const float4*>(part + q * slice + e));
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        if (mask) {
+            const uint32_t mw = *reinterpret_cast<const uint32_t*>(mask + (long long)row_pat[row] * mask_ld + col);
+            if (!(mw & 0xFFu)) a.x = 0.f;
+            if (!(mw & 0xFF00u)) a.y = 0.f;
+            if (!(mw & 0xFF0000u)) a.z = 0.f;
+            if (!(mw & 0xFF000000u)) a.w = 0.f;
+        }
+        if (out_bf16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+            uint2 w;
+            w.x = *reinterpret_cast<uint32_t*>(&lo);
+            w.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + row * ldo + col) = w;
+        } else {
+            *reinterpret_cast<float4*>(static_cast<float*>(out) + row * ldo + col) = a;
+        }
+    }
+}
+
+// S K-slices and the tile width: wide tiles (each A row block read by few N
+// tiles), K split until the slices cover the SMs.  1 = do not split.
+static int splitk_plan(const UmmaSpec& s, int* bn_out, int* kslice_out) {
+    static const int env_max = [] {
+        const char* e = getenv("PG_UMMA_SPLITK");  // max K slices (1 disables)
+        return e ? std::max(1, atoi(e)) : UM_MAX_GROUPS;
+    }();
+    int dev = 0, sms = 0;
+    PG_CUDA_THROW(cudaGetDevice(&dev));
+    PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const bool pairs = umma_pairs_enabled() != 0 && s.M >= 2 * UM_BM;
+    const int rows = pairs ? 2 * UM_BM : UM_BM, slots = pairs ? sms / 2 : sms;
+    int bn = pick_bn(s.N);
+    if (pairs) bn = std::min(UM_BN_MAX, (bn + 31) / 32 * 32);
+    const long tiles = (long)((s.M + rows - 1) / rows) * ((s.N + bn - 1) / bn);
+    static const int kmin = [] {  // measured: only the long-K GEMMs gain (down's stage 1, K = 11008)
+        const char* e = getenv("PG_UMMA_SPLITK_KMIN");
+        return e ? atoi(e) : 8192;
+    }();
+    if (s.N % 4 || s.ldo % 4 || tiles * 2 > (long)slots || s.K < kmin) return 1;
+    int S = (int)(slots / tiles);
+    S = std::min(S, std::max(1, s.K / 512));  // >= 8 k-blocks per slice
+    S = std::min(S, std::min(UM_MAX_GROUPS, env_max));
+    if (S <= 1) return 1;
+    const int ks = (s.K + S - 1) / S;
+    const int kslice = (ks + UM_BK - 1) / UM_BK * UM_BK;
+    *bn_out = bn;
+    *kslice_out = kslice;
+    return (s.K + kslice - 1) / kslice;
+}
+
+size_t umma_splitk_bytes(const UmmaSpec& s) {
+    int bn = 0, ks = 0;
+    const int S = splitk_plan(s, &bn, &ks);
+    return S > 1 ? (size_t)S * s.M * s.N * 4 : 0;
+}
+
+bool launch_umma_splitk(const UmmaSpec& s, void* ws, cudaStream_t st) {
+    return launch_umma_splitk_multi({s}, ws, st);
+}
+
+bool launch_umma_splitk_multi(const std::vector<UmmaSpec>& specs, void* ws, cudaStream_t st) {
+    std::vector<int> Ss, bns, kss;
+    for (const UmmaSpec& s : specs) {
+        int bn = 0, ks = 0;
+        const int S = splitk_plan(s, &bn, &ks);
+        if (S <= 1) return false;  // all or nothing: one grouped launch of every slice
+        Ss.push_back(S);
+        bns.push_back(bn);
+        kss.push_back(ks);
+    }
+    if (ws == nullptr) return false;
+    std::vector<UmmaSpec> parts;
+    std::vector<float*> pws;
+    float* w = static_cast<float*>(ws);
+    for (size_t j = 0; j < specs.size(); ++j) {
+        const UmmaSpec& s = specs[j];
+        pws.push_back(w);
+        for (int q = 0; q < Ss[j]; ++q) {
+            const int k0 = q * kss[j];
+            UmmaSpec p = s;
+            p.a = static_cast<const __nv_bfloat16*>(s.a) + k0;
+            p.b = static_cast<const __nv_bfloat16*>(s.b) + k0;
+            p.K = std::min(kss[j], s.K - k0);
+            p.out = w + (size_t)q * s.M * s.N;
+            p.ldo = s.N;
+            p.out_bf16 = 0;
+            p.mask = nullptr;
+            p.row_pat = nullptr;
+            p.bn = bns[j];
+            p.direct_epi = 1;
+            parts.push_back(p);
+        }
+        w += (size_t)Ss[j] * s.M * s.N;
+    }
+    launch_umma(parts, st);
+    int dev = 0, sms = 0;
+    PG_CUDA_THROW(cudaGetDevice(&dev));
+    PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (size_t j = 0; j < specs.size(); ++j) {
+        const UmmaSpec& s = specs[j];
+        const long long n4 = (long long)s.M * s.N / 4;
+        const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)sms * 8);
+        k_splitk_reduce<<<blocks, 256, 0, st>>>(pws[j], Ss[j], s.M, s.N, s.mask, s.mask_ld, s.row_pat, s.out, s.ldo,
+                                                s.out_bf16);
+        PG_LAUNCH_CHECK();
+    }
+    return true;
 }
 
 }  // namespace pg

@@ -25,7 +25,19 @@ struct UmmaSpec {
     const int32_t* row_pat = nullptr;
     int b_rows = 0;  // rows of the B operand in memory (0: N); rows in [b_rows, N) read as zero
     int bn = 0;      // tile width override (0: chosen by launch_umma)
+    int direct_epi = 0;  // CTA-pair kernel: store from registers instead of the TMA-store epilogue
 };
+
+// C = A . B^T with K split across CTAs when the M x N tiles cannot cover the
+// SMs without re-reading the A operand once per narrow N tile (small-batch
+// GEMMs with long K): S K-slices run as one grouped launch into f32 partials
+// (register-store epilogue: the tiles are short), then one kernel sums them in
+// slice order (deterministic), applies the row mask and converts.  Returns
+// false (and launches nothing) when splitting does not pay; workspace bytes
+// from umma_splitk_bytes.
+size_t umma_splitk_bytes(const UmmaSpec& s);
+bool launch_umma_splitk(const UmmaSpec& s, void* workspace, cudaStream_t st);
+bool launch_umma_splitk_multi(const std::vector<UmmaSpec>& specs, void* workspace, cudaStream_t st);
 
 
 

@@ -116,7 +116,8 @@ def _union_ref(A, B, masks, pid, X):
 
 
 @pytest.mark.parametrize("m,n,r,K,P,T", [(1000, 1024, 768, 384, 6, 300), (4096, 4096, 1638, 819, 256, 256),
-                                         (11008, 4096, 2388, 1194, 64, 256), (384, 512, 300, 150, 3, 5)])
+                                         (11008, 4096, 2388, 1194, 64, 256), (384, 512, 300, 150, 3, 5),
+                                         (4096, 11008, 2388, 1194, 32, 256)])  # last: long K, split-K path
 def test_union_masked_batch(pg, port, m, n, r, K, P, T):
     """config 4: a heterogeneous decode batch (every token with its prompt's
     selection) through one pass over the weights equals masked_forward per
