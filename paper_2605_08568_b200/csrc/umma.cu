@@ -309,7 +309,8 @@ constexpr int U2_A_BYTES = UM_BM * UM_BK * 2;                 // 16 KB (this CTA
 constexpr int U2_B_BYTES = (UM_BN_MAX / 2) * UM_BK * 2;       // 16 KB (this CTA's BN/2 rows)
 constexpr int U2_STAGE_BYTES = U2_A_BYTES + U2_B_BYTES;
 constexpr int U2_OUT_BYTES = 32 * 32 * 4;  // one 32 x 32 output chunk (f32 worst case)
-constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 256 + 4 * 2 * U2_OUT_BYTES;
+// [align slack 1 KB][ring][barriers, 1 KB][per-warp output staging]
+constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 1024 + 4 * 2 * U2_OUT_BYTES;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
