@@ -113,3 +113,20 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in txt.replace("oracle_", "").lower() or f == "_build.py", f
+
+
+def test_peer_buffer_sizing_and_validation(pglib):
+    """Expert-sharded peer reduction: receive buffers hold 2 parities x npeer x m
+    tagged 8-byte words; 1..8 ranks."""
+    import ctypes as C
+    from paper_2605_08568_b200 import _lib
+    out = C.c_size_t()
+    _lib.call("pg_peer_buffer_bytes", 4096, 4, C.byref(out))
+    assert out.value == 2 * 4 * 4096 * 8
+    with pytest.raises(ValueError, match="1..8 ranks"):
+        _lib.call("pg_peer_buffer_bytes", 4096, 9, C.byref(out))
+    with pytest.raises(ValueError, match="1..8 ranks"):
+        _lib.call("pg_peer_buffer_bytes", 0, 2, C.byref(out))
+    from paper_2605_08568_b200.dist import PeerReduceLinear
+    with pytest.raises(ValueError, match="1..8 ranks"):
+        PeerReduceLinear(np.zeros((4, 4)), np.zeros((4, 4)), 9, 0)
