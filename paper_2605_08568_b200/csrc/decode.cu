@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             par ^= 1u << k;
             const Desc& D = descs[k];
             const int cnt = D.count, g0 = D.gidx, last = D.last, l = D.lin;
+            if (cnt && ph == 1) STAMP(14);  // phase-1 stage-1 data seen (last write wins)
             if (cnt) {
                 const LinS& Ls = L[l];
                 const int rb = (int)Ls.ldb_b;

@@ -76,13 +76,13 @@ def stamps():
     a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16)[:148].astype(np.int64)
     t0 = a[:, 0].min()
     names = ["start", "x0", "s1done0", "bar0", "z0", "s2done0", "xstaged0", "x1", "s1done1", "bar1", "z1", "s2done1",
-             "prod_done", "end"]
+             "prod_done", "end", "s1data1"]
     for k, nm in enumerate(names):
         col = a[:, k]
         if (col > 0).all():
             print(f"{nm:9s} min {(col.min() - t0) / 1e3:7.2f} med {(np.median(col) - t0) / 1e3:7.2f} "
                   f"max {(col.max() - t0) / 1e3:7.2f} us")
-            if nm in ("start", "s1done0", "s2done0", "s1done1", "prod_done") and os.environ.get("EXP_LATE"):
+            if nm in ("start", "s1done0", "s2done0", "s1done1", "prod_done", "s1data1") and os.environ.get("EXP_LATE"):
                 late = np.argsort(col)[-8:][::-1]
                 print("    latest CTAs:", [(int(c), round((col[c] - t0) / 1e3, 2)) for c in late])
 
