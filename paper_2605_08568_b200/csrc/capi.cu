@@ -645,6 +645,13 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
         return e ? atoi(e) : -2;
     }();
     P.throttle = throttle_env != -2 ? throttle_env : (mlp ? 3 : -1);
+    // weights are streamed once per launch: L2 evict-first keeps them from
+    // displacing the exchange words (measured -2 % per MLP step)
+    static const int l2hint_env = [] {
+        const char* e = getenv("PG_CHAIN_L2HINT");
+        return e ? atoi(e) : 1;
+    }();
+    P.l2hint = l2hint_env;
     P.dbg = chain_debug_buffer();
     const size_t zw = wdt == PG_F64 ? 2 : 1;  // tagged exchange words per z value
     size_t zbytes = 256;

@@ -52,6 +52,7 @@ struct ChainParams {
     // each CTA sums its own rows over the ranks in rank order -- compute and
     // all-reduce in one kernel, no fence (the tag is in the data word)
     int throttle;  // >= 0: after a stage-1 segment, at most this many chunks until the z exchange is done
+    int l2hint;    // 1: weight copies carry an L2 evict-first policy
     int npeer, prank;
     unsigned long long* peer_recv[kMaxPeers];
 };

@@ -102,6 +102,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+// streamed-once weights: evict-first in L2 so they do not displace the exchange words
+__device__ __forceinline__ void bulk_g2s_ef(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void consumer_sync() {  // named barrier over the 15 consumer warps
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
 }
@@ -348,10 +354,13 @@ __device__ void chain_producer(const ChainParams& P, const LinS* lins, Desc* des
         k = (k + 1 == nst) ? 0 : k + 1;
         d = nullptr;
     };
+    uint64_t pol = 0;
+    if (P.l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     auto copy = [&](const char* src, int bytes) {
         const uint32_t bar = smem_u32(&full[k]);
         mbar_expect_tx(bar, (uint32_t)bytes);
-        bulk_g2s(smem_u32(ring + (size_t)k * CH + c_used), src, (uint32_t)bytes, bar);
+        if (P.l2hint) bulk_g2s_ef(smem_u32(ring + (size_t)k * CH + c_used), src, (uint32_t)bytes, bar, pol);
+        else bulk_g2s(smem_u32(ring + (size_t)k * CH + c_used), src, (uint32_t)bytes, bar);
         c_used += bytes;
     };
     for (int ph = 0; ph < P.nphase; ++ph) {
