@@ -908,7 +908,11 @@ int pg_masked_forward_union(pg_layer L, const uint8_t* masks, size_t P, const in
     s1.mask_ld = (long long)sel_mask_ld(L->r);
     s1.row_pat = tok_pat;
     s1.b_rows = L->r;
-    const UmmaSpec s2{z.p, rp, L->a, L->lda, y, L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0};
+    s1.a_hint = 2;  // the batch's tokens are re-read per N tile: keep them in L2
+    s1.b_hint = 1;  // every weight byte is read once per batch: evict first
+    UmmaSpec s2{z.p, rp, L->a, L->lda, y, L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0};
+    s2.a_hint = 2;
+    s2.b_hint = 1;
     // long K with few tiles: split K across the SMs (f32 partials), else narrow tiles
     Scratch ws(std::max(umma_splitk_bytes(s1), umma_splitk_bytes(s2)), st);
     if (!launch_umma_splitk(s1, ws.p, st)) launch_umma({s1}, st);
@@ -945,8 +949,13 @@ int pg_module_forward_union(const pg_layer* Ls, const uint8_t* const* masks, con
         a.mask_ld = (long long)sel_mask_ld(L->r);
         a.row_pat = tok_pat;
         a.b_rows = L->r;
+        a.a_hint = 2;  // tokens re-read per N tile: keep; weights read once: evict first
+        a.b_hint = 1;
         s1.push_back(a);
-        s2.push_back(UmmaSpec{zl, rp, L->a, L->lda, ys[l], L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0});
+        UmmaSpec b{zl, rp, L->a, L->lda, ys[l], L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0};
+        b.a_hint = 2;
+        b.b_hint = 1;
+        s2.push_back(b);
     }
     // the linears' first GEMMs share x: one grouped launch per stage (with
     // their K split across the SMs when that pays, see launch_umma_splitk)

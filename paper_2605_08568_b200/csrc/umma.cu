@@ -48,6 +48,7 @@ struct UmmaGroup {
     long long mask_ld;
     const int32_t* row_pat;
     int direct_epi;
+    int a_hint, b_hint;
 };
 
 // Passed as one __grid_constant__ parameter block (< 32 KB): TMA reads the
@@ -82,6 +83,18 @@ __device__ __forceinline__ void u_tma_2d(uint32_t dst, const CUtensorMap* map, i
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
         "l"(map), "r"(x), "r"(y), "r"(bar)
         : "memory");
+}
+// operand loads with an L2 policy (pol: createpolicy result)
+__device__ __forceinline__ void u_tma_2d_h(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                           uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(map), "r"(x), "r"(y), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t u_policy(int hint, uint64_t first, uint64_t last) {
+    return hint == 1 ? first : last;
 }
 __device__ __forceinline__ uint64_t u_desc(uint32_t saddr) {
     // K-major, 128B swizzle: LBO=1 (unused), SBO=1024B, version 1 (sm100), layout 2
@@ -221,6 +234,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
+            uint64_t pf, pl;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
@@ -236,8 +252,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped(const __grid_con
                     const uint32_t fb = u_smem(&full[s]);
                     u_mbar_arrive_tx(fb, bytes);
                     unsigned char* st = base + s * UM_STAGE_BYTES;
-                    u_tma_2d(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
-                    u_tma_2d(u_smem(st + UM_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
+                    if (G.a_hint) u_tma_2d_h(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb, u_policy(G.a_hint, pf, pl));
+                    else u_tma_2d(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
+                    if (G.b_hint)
+                        u_tma_2d_h(u_smem(st + UM_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb,
+                                   u_policy(G.b_hint, pf, pl));
+                    else u_tma_2d(u_smem(st + UM_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
                     if (++s == UM_STAGES) { s = 0; ph ^= 1; }
                 }
             }
@@ -336,6 +356,14 @@ __device__ __forceinline__ void u_tma_2d_pair(uint32_t dst, const CUtensorMap* m
     asm volatile(
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
         ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void u_tma_2d_pair_h(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                                uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void u_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
@@ -456,6 +484,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
         // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
+            uint64_t pf, pl;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
             int s = 0;
             uint32_t ph = 0;
             for (int t = pair; t < P.total_tiles; t += npairs) {
@@ -472,8 +503,13 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
                     const uint32_t fb = leader_addr(u_smem(&full[s]));
                     if (leader) u_mbar_arrive_tx_cluster(fb, bytes);
                     unsigned char* st = base + s * U2_STAGE_BYTES;
-                    u_tma_2d_pair(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
-                    u_tma_2d_pair(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
+                    if (G.a_hint)
+                        u_tma_2d_pair_h(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb, u_policy(G.a_hint, pf, pl));
+                    else u_tma_2d_pair(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
+                    if (G.b_hint)
+                        u_tma_2d_pair_h(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb,
+                                        u_policy(G.b_hint, pf, pl));
+                    else u_tma_2d_pair(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
                     if (++s == U2_STAGES) { s = 0; ph ^= 1; }
                 }
             }
@@ -665,6 +701,12 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
             P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
                                           pairs ? G.bn / 2 : G.bn);
+            static const int hints_env = [] {
+                const char* e = getenv("PG_UMMA_L2HINT");
+                return e ? atoi(e) : 1;
+            }();
+            G.a_hint = hints_env ? s.a_hint : 0;
+            G.b_hint = hints_env ? s.b_hint : 0;
             G.direct_epi = s.direct_epi;
             G.mask = s.mask;
             G.mask_ld = s.mask_ld;

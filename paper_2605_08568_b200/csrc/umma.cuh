@@ -25,6 +25,7 @@ struct UmmaSpec {
     const int32_t* row_pat = nullptr;
     int b_rows = 0;  // rows of the B operand in memory (0: N); rows in [b_rows, N) read as zero
     int bn = 0;      // tile width override (0: chosen by launch_umma)
+    int a_hint = 0, b_hint = 0;  // L2 policy of the operand loads: 0 default, 1 evict-first, 2 evict-last
     int direct_epi = 0;  // CTA-pair kernel: store from registers instead of the TMA-store epilogue
 };
 
