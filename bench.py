@@ -438,6 +438,8 @@ def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct
     launches = pg.launch_count() - n0
     reps = 5
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
     with torch.cuda.stream(st):
         gr.replay()
         e0.record(st)
@@ -445,7 +447,7 @@ def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct
             gr.replay()
         e1.record(st)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    ms = max_over_ranks_ms(torch, e0.elapsed_time(e1) / reps, dev, world)
     byt = layers * sum(dims[i][0] * (m + n) * 2 for i, (m, n) in enumerate(lin.values()))
     fl = layers * 2 * P * sum(dims[i][0] * (m + n) for i, (m, n) in enumerate(lin.values()))
     return {"workload": f"config4: {layers}-layer LLaMA-7B-shaped stack, {P} prompts x 1 decode token, "
@@ -456,6 +458,15 @@ def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct
             "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": byt / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": byt,
                          "tensor_tflops": fl / (ms * 1e-3) / 1e12}}
+
+
+def max_over_ranks_ms(torch, ms, dev, world):
+    """Device time of a secondary arm: the slowest rank's (like the headline)."""
+    if world <= 1:
+        return ms
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
 
 
 def prefill_arm(pg, torch, dev, world, P=16, T=2048):
@@ -497,12 +508,14 @@ def prefill_arm(pg, torch, dev, world, P=16, T=2048):
         route_all()
     torch.cuda.synchronize()
     route_reps = 5
+    if world > 1:
+        torch.distributed.barrier()
     e0.record()
     for _ in range(route_reps):
         route_all()
     e1.record()
     torch.cuda.synchronize()
-    route_ms = e0.elapsed_time(e1) / route_reps
+    route_ms = max_over_ranks_ms(torch, e0.elapsed_time(e1) / route_reps, dev, world)
     # pack each prompt's experts once (serving: after routing / a cache hit)
     t0 = time.perf_counter()
     aggs = {nm: [pg.aggregate_layout(layers[nm][0], [pg.RankSelection(sels[nm][p].cpu().numpy())], PSI)
@@ -518,12 +531,14 @@ def prefill_arm(pg, torch, dev, world, P=16, T=2048):
         layer_step()
     torch.cuda.synchronize()
     reps = 5
+    if world > 1:
+        torch.distributed.barrier()
     e0.record()
     for _ in range(reps):
         layer_step()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    ms = max_over_ranks_ms(torch, e0.elapsed_time(e1) / reps, dev, world)
     _, tflops_peak, peak_kind = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
     return {"workload": "config3: LLaMA-7B decoder layer (q,k,v,o,gate,up,down) ratio 0.6, 16 prompts x 2048 "
