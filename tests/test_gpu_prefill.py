@@ -172,3 +172,24 @@ def test_module_forward_union_grouped_equals_single(pg, port):
     ys = pg.module_forward_union(Ls, Bs, pid, X)
     for L, b, y in zip(Ls, Bs, ys):
         assert torch.equal(y, pg.masked_forward_union(L, b, pid, X))
+
+
+def test_union_masked_batch_f32_out_and_long_batch(pg, port):
+    """f32 output and a long heterogeneous batch (T = 1024: several M tiles of
+    CTA pairs) through the union path, vs the fp32 reference of the same math."""
+    from oracle import pyoracle
+    m, n, r, K, P, T = 2048, 1024, 640, 320, 40, 1024
+    A, B = layer_data(port, m, n, r, 77)
+    pats = [p[0] for p in pyoracle.make_patterns(9090, P, [(r, K)])]
+    L = pg.FactorizedLayer(A, B, K, dtype="bf16")
+    batch = pg.SelectionBatch(L, [pg.RankSelection(p) for p in pats])
+    pid = np.random.default_rng(11).integers(0, P, T)
+    X = torch.from_numpy(port.gaussian(78, (T, n))).cuda().to(torch.bfloat16)
+    Y = pg.masked_forward_union(L, batch, torch.from_numpy(pid.astype(np.int32)).cuda(), X, out_dtype=torch.float32)
+    assert Y.dtype == torch.float32 and Y.shape == (T, m)
+    masks = np.zeros((P, r), np.float32)
+    for p, s in enumerate(pats):
+        masks[p, s] = 1.0
+    assert rel(Y.cpu().numpy(), _union_ref(A, B, masks, pid, X)) <= 2e-3
+    Yb = pg.masked_forward_union(L, batch, pid, X)  # bf16 output: the same values rounded
+    assert rel(Yb.float().cpu().numpy(), Y.cpu().numpy()) <= 1e-2
