@@ -366,6 +366,26 @@ __device__ __forceinline__ void u_tma_2d_pair_h(uint32_t dst, const CUtensorMap*
         ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar), "l"(pol)
         : "memory");
 }
+// ---- k_umma_grouped4 (PG_UMMA_MC=1, off by default): clusters of two CTA
+// pairs on consecutive M tiles of one N tile; each CTA loads a quarter of the
+// B tile and multicasts it to its counterpart in the other pair, so per SM the
+// B bytes per flop halve.  Measured: +9 % TFLOP/s per SM, but only 33 clusters
+// of 4 fit (132 SMs) against 74 pairs (148 SMs), so whole-GPU throughput is
+// equal or lower (profiles/r1_prefill_config3.txt).  Parity tests pass with it.
+// B quarter tile multicast to the same-parity CTA of both pairs of a 4-CTA cluster
+__device__ __forceinline__ void u_tma_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                                 uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void u_commit2_mask(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"(mask)
+                 : "memory");
+}
 __device__ __forceinline__ void u_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -573,6 +593,138 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+__global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped4(const __grid_constant__ UmmaParams P) {
+    extern __shared__ __align__(1024) unsigned char usmem[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(usmem) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + U2_STAGES * U2_STAGE_BYTES);
+    uint64_t* full = bars;                        // [STAGES] (used in the leader)
+    uint64_t* empty = bars + U2_STAGES;           // [STAGES] (each CTA)
+    uint64_t* tfull = bars + 2 * U2_STAGES;       // [2] (each CTA)
+    uint64_t* tempty = bars + 2 * U2_STAGES + 2;  // [2] (used in the leader: both CTAs' epilogues)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * U2_STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // cluster of two CTA pairs: ranks {0,1} and {2,3}; both pairs work on the
+    // same N tile (consecutive M tiles) and share its B tile: each CTA loads a
+    // quarter of the B rows and multicasts it to its counterpart in the other pair
+    const uint32_t crank = cluster_rank();
+    const uint32_t rank = crank & 1u, pp = crank >> 1;
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 2, npairs = gridDim.x >> 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < U2_STAGES; ++s) {
+            u_mbar_init(u_smem(&full[s]), 1);
+            u_mbar_init(u_smem(&empty[s]), 2);  // both pairs' MMAs read this stage's B
+        }
+        for (int a = 0; a < 2; ++a) {
+            u_mbar_init(u_smem(&tfull[a]), 1);
+            u_mbar_init(u_smem(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // same warp in both CTAs: 2 accumulators x 256 columns
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(u_smem(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see k_umma_grouped
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (both CTAs)
+        if (lane == 0) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            uint64_t pf, pl;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = pair; t < P.total_tiles; t += npairs) {
+                int g = 0;
+                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+                const UmmaGroup& G = P.groups[g];
+                const int lt = t - G.tile_base;
+                const int m0 = (lt % G.tiles_m) * 4 * UM_BM + (int)pp * 2 * UM_BM + (int)rank * UM_BM;
+                const int nq = (lt / G.tiles_m) * G.bn + (int)rank * (G.bn / 2) + (int)pp * (G.bn / 4);
+                const uint16_t mc = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+                const int kbs = (G.K + UM_BK - 1) / UM_BK;
+                const uint32_t bytes = 2 * (UM_A_BYTES + (uint32_t)(G.bn / 2) * UM_BK * 2);  // both CTAs
+                for (int kb = 0; kb < kbs; ++kb) {
+                    u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
+                    const uint32_t fb = leader_addr(u_smem(&full[s]));
+                    if (leader) u_mbar_arrive_tx_cluster(fb, bytes);
+                    unsigned char* st = base + s * U2_STAGE_BYTES;
+                    if (G.a_hint)
+                        u_tma_2d_pair_h(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb, u_policy(G.a_hint, pf, pl));
+                    else u_tma_2d_pair(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
+                    u_tma_2d_pair_mc(u_smem(st + U2_A_BYTES + pp * (G.bn / 4) * UM_BK * 2), &P.maps[2 * g + 1],
+                                     kb * UM_BK, nq, fb, mc);
+                    if (++s == U2_STAGES) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (leader && lane == 0) {
+            int s = 0, acc = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int t = pair; t < P.total_tiles; t += npairs) {
+                int g = 0;
+                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+                const UmmaGroup& G = P.groups[g];
+                const int kbs = (G.K + UM_BK - 1) / UM_BK;
+                const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(G.bn >> 3) << 17) |
+                                       ((uint32_t)((2 * UM_BM) >> 4) << 24);
+                u_mbar_wait(u_smem(&tempty[acc]), aph ^ 1);  // both CTAs drained this accumulator
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(acc * UM_BN_MAX);
+                for (int kb = 0; kb < kbs; ++kb) {
+                    u_mbar_wait(u_smem(&full[s]), ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = u_smem(base + s * U2_STAGE_BYTES), sb = sa + U2_A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < UM_BK / 16; ++k)
+                        u_mma2(d, u_desc(sa + k * 32), u_desc(sb + k * 32), idesc, (kb | k) != 0);
+                    u_commit2_mask(u_smem(&empty[s]), 0xF);  // this pair is done with the stage (all 4 CTAs)
+                    if (++s == U2_STAGES) { s = 0; ph ^= 1; }
+                }
+                u_commit2_mask(u_smem(&tfull[acc]), (uint16_t)(3u << (2 * pp)));  // accumulator ready in this pair
+                if (++acc == 2) { acc = 0; aph ^= 1; }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2-5, both CTAs)
+        const int q = warp & 3;
+        unsigned char* ostage = base + U2_STAGES * U2_STAGE_BYTES + 1024 + (q) * 2 * U2_OUT_BYTES;
+        int nbuf = 0;
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = pair; t < P.total_tiles; t += npairs) {
+            int g = 0;
+            while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+            const UmmaGroup& G = P.groups[g];
+            const int lt = t - G.tile_base;
+            const int m0 = (lt % G.tiles_m) * 4 * UM_BM + (int)pp * 2 * UM_BM + (int)rank * UM_BM,
+                      n0 = (lt / G.tiles_m) * G.bn;
+            u_mbar_wait(u_smem(&tfull[acc]), aph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int row = m0 + q * 32 + lane;
+            if (G.direct_epi) epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
+            else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf);
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
+            if (++acc == 2) { acc = 0; aph ^= 1; }
+        }
+    }
+    if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores out of smem
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -647,6 +799,8 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
     if (!attr) {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr = true;
     }
     // CTA pairs for batches whose every GEMM has at least 256 rows
@@ -661,6 +815,11 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
         const int ng = (int)std::min<size_t>(UM_MAX_GROUPS, specs.size() - g0);
         auto P = std::make_unique<UmmaParams>();
         int tiles = 0;
+        static const int mc_env = [] {  // experiments: clusters of two CTA pairs sharing B by multicast
+            const char* e = getenv("PG_UMMA_MC");
+            return e ? atoi(e) : 0;
+        }();
+        const bool mc = pairs && mc_env != 0;
         // few tiles (small-batch decode through the tensor cores): one narrower
         // tile width for the whole launch until the SMs are covered, minimising
         // waves x tile width (time per tile ~ bn x K)
@@ -700,7 +859,7 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             else if (common_bn > 0) G.bn = std::min(G.bn, common_bn);
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
             P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
-                                          pairs ? G.bn / 2 : G.bn);
+                                          mc ? G.bn / 4 : (pairs ? G.bn / 2 : G.bn));
             static const int hints_env = [] {
                 const char* e = getenv("PG_UMMA_L2HINT");
                 return e ? atoi(e) : 1;
@@ -718,7 +877,7 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             G.N = s.N;
             G.K = s.K;
             G.out_bf16 = s.out_bf16;
-            G.tiles_m = (s.M + (pairs ? 2 * UM_BM : UM_BM) - 1) / (pairs ? 2 * UM_BM : UM_BM);
+            G.tiles_m = (s.M + (mc ? 4 * UM_BM : (pairs ? 2 * UM_BM : UM_BM)) - 1) / (mc ? 4 * UM_BM : (pairs ? 2 * UM_BM : UM_BM));
             G.tiles_n = (s.N + G.bn - 1) / G.bn;
             G.tile_base = tiles;
             tiles += G.tiles_m * G.tiles_n;
@@ -726,7 +885,41 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
         P->ngroups = ng;
         P->total_tiles = tiles;
         if (tiles == 0) continue;
-        if (pairs) {
+        if (mc) {
+            static int max_cl = [&] {
+                cudaLaunchConfig_t q = {};
+                q.gridDim = dim3((unsigned)(sms / 4 * 4));
+                q.blockDim = dim3(UM_THREADS);
+                q.dynamicSmemBytes = U2_SMEM;
+                cudaLaunchAttribute a[1];
+                a[0].id = cudaLaunchAttributeClusterDimension;
+                a[0].val.clusterDim.x = 4;
+                a[0].val.clusterDim.y = 1;
+                a[0].val.clusterDim.z = 1;
+                q.attrs = a;
+                q.numAttrs = 1;
+                int n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, k_umma_grouped4, &q) != cudaSuccess || n <= 0) n = sms / 4;
+                if (getenv("PG_UMMA_DEBUG")) fprintf(stderr, "umma4: max active clusters %d\n", n);
+                return n;
+            }();
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(4 * std::min(tiles, max_cl)));
+            cfg.blockDim = dim3(UM_THREADS);
+            cfg.dynamicSmemBytes = U2_SMEM;
+            cfg.stream = st;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 4;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[1].val.programmaticStreamSerializationAllowed = umma_pdl();
+            cfg.attrs = at;
+            cfg.numAttrs = 2;
+            PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped4, *P));
+            count_launch();
+        } else if (pairs) {
             // persistent: only as many pairs as can be co-resident (cluster
             // placement needs both SMs of a TPC free)
             static int max_pairs = [&] {
