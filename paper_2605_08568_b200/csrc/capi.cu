@@ -6,6 +6,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "chain.cuh"
@@ -551,12 +552,14 @@ struct LinSpec {
 // Decode-chain workspace per (device, stream): [barrier counter | z | act].
 // Grows outside graph capture only; reused by every launch on that stream.
 static std::mutex g_ws_mu;
-static std::map<std::pair<int, cudaStream_t>, std::pair<char*, size_t>> g_ws;
-static char* chain_workspace(cudaStream_t st, size_t bytes) {
+// keyed by (device, stream, grid size): the monotone barrier counter and the
+// launch epoch count in units of the grid size, so each grid size keeps its own
+static std::map<std::tuple<int, cudaStream_t, int>, std::pair<char*, size_t>> g_ws;
+static char* chain_workspace(cudaStream_t st, size_t bytes, int grid) {
     int dev = 0;
     PG_CUDA_THROW(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    auto& w = g_ws[{dev, st}];
+    auto& w = g_ws[std::make_tuple(dev, st, grid)];
     if (w.second < bytes) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         PG_CUDA_THROW(cudaStreamIsCapturing(st, &cs));
@@ -663,7 +666,17 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
     // size) and z words carry their launch's tag, so consecutive chain launches
     // need no memset between them and can overlap under programmatic dependent
     // launch.
-    char* base = chain_workspace(st, zbytes + act_bytes);
+    static const int grid_env = [] {  // experiments: decode-chain grid size (default: every SM)
+        const char* e = getenv("PG_CHAIN_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    // MLP launches leave 4 SMs free: the next launch's first CTAs (programmatic
+    // dependent launch) start streaming their weights during this launch's tail
+    // (measured ~1 % per step on three boxes)
+    int grid = grid_env ? grid_env : (mlp ? std::max(1, chain_grid() - 4) : 0);
+    if (peer && peer->npeer > 0) grid = peer->grid;
+    const int eff_grid = grid > 0 ? std::min(grid, chain_grid()) : chain_grid();
+    char* base = chain_workspace(st, zbytes + act_bytes, eff_grid);
     P.bar = reinterpret_cast<unsigned long long*>(base);
     P.epoch = reinterpret_cast<unsigned long long*>(base + 64);
     // measured: tagged z words win for the 2-phase MLP launch (30.5 vs 31.7 us
@@ -691,16 +704,10 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
             off += round_up((size_t)S.cap * zw * 8, 256);
         }
     }
-    static const int grid_env = [] {  // experiments: decode-chain grid size (default: every SM)
-        const char* e = getenv("PG_CHAIN_GRID");
-        return e ? atoi(e) : 0;
-    }();
-    int grid = grid_env;
     if (peer && peer->npeer > 0) {
         P.npeer = peer->npeer;
         P.prank = peer->rank;
         for (int r = 0; r < peer->npeer; ++r) P.peer_recv[r] = static_cast<unsigned long long*>(peer->bufs[r]);
-        grid = peer->grid;
     }
     const size_t total = 1024 + xs_bytes + zs_bytes + kRingStages * (128 + 16) + 128 + (size_t)kRingStages * ch;
     launch_chain(wdt, P, std::min(total, (size_t)227 * 1024), st, grid);
