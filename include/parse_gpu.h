@@ -300,6 +300,12 @@ int pg_fill_normal_device(void* out_dev, pg_dtype dtype, size_t count, uint64_t 
  * per-token H2D of x and D2H of y without copy-engine nodes in the step. */
 int pg_copy_io(const void* src, void* dst, size_t bytes, pg_stream stream);
 
+/* Release the per-stream workspaces the library keeps per (device, stream,
+ * grid size) for `stream` (decode chain: barrier counter, launch epoch, z/act
+ * exchange words; union batch: launch epoch, split-tile flags and partials); call before destroying a per-request stream.  Synchronises the
+ * stream first.  The next chain launch on that stream re-creates them. */
+int pg_chain_workspace_release(pg_stream stream);
+
 /* Diagnostics: with PG_CHAIN_DBG=1 the decode-chain kernel records per-CTA
  * %globaltimer stamps [cta][16] of its phases; copies the last launch's. */
 int pg_chain_debug_dump(uint64_t* out_host, size_t n);

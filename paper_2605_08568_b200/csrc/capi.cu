@@ -11,6 +11,7 @@
 
 #include "chain.cuh"
 #include "umma.cuh"
+#include "union_wm.cuh"
 
 namespace pg {
 
@@ -549,17 +550,24 @@ struct LinSpec {
 // Single-launch decode chain (decode.cu).  phases[0] = linears sharing x; when
 // mlp is set, phase 0 is {up, gate} with the silu epilogue into act and phase
 // 1 is {down} reading act.
-// Decode-chain workspace per (device, stream): [barrier counter | z | act].
-// Grows outside graph capture only; reused by every launch on that stream.
+// Decode-chain workspace per (device, stream, grid size): [barrier counter |
+// epoch | z | act].  Grows outside graph capture only; reused by every launch
+// on that stream with that grid.  Keyed by grid size because the monotone
+// barrier counter and the launch epoch count in units of the grid size.
+// pg_chain_workspace_release(stream) frees a stream's workspaces (call it
+// before destroying a per-request stream).
 static std::mutex g_ws_mu;
-// keyed by (device, stream, grid size): the monotone barrier counter and the
-// launch epoch count in units of the grid size, so each grid size keeps its own
-static std::map<std::tuple<int, cudaStream_t, int>, std::pair<char*, size_t>> g_ws;
-static char* chain_workspace(cudaStream_t st, size_t bytes, int grid) {
+// `owner` separates workspaces whose launch epochs must advance independently
+// of other chain launches on the same stream: the expert-sharded peer path keys
+// its workspace by this rank's receive buffer, so its tags count only that
+// PeerReduceLinear's launches (identical on every rank) and an unrelated chain
+// launch on one rank cannot desynchronise the ranks' tags.
+static std::map<std::tuple<int, cudaStream_t, int, const void*>, std::pair<char*, size_t>> g_ws;
+static char* chain_workspace(cudaStream_t st, size_t bytes, int grid, const void* owner = nullptr) {
     int dev = 0;
     PG_CUDA_THROW(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    auto& w = g_ws[std::make_tuple(dev, st, grid)];
+    auto& w = g_ws[std::make_tuple(dev, st, grid, owner)];
     if (w.second < bytes) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         PG_CUDA_THROW(cudaStreamIsCapturing(st, &cs));
@@ -569,7 +577,9 @@ static char* chain_workspace(cudaStream_t st, size_t bytes, int grid) {
         if (w.first) PG_CUDA_THROW(cudaFree(w.first));
         const size_t sz = round_up(bytes, 1 << 20);
         PG_CUDA_THROW(cudaMalloc(&w.first, sz));
-        PG_CUDA_THROW(cudaMemset(w.first, 0, sz));
+        // on the launching stream: a user stream created non-blocking is not
+        // ordered after the legacy default stream a plain cudaMemset runs on
+        PG_CUDA_THROW(cudaMemsetAsync(w.first, 0, sz, st));
         w.second = sz;
     }
     return w.first;
@@ -676,7 +686,8 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
     int grid = grid_env ? grid_env : (mlp ? std::max(1, chain_grid() - 4) : 0);
     if (peer && peer->npeer > 0) grid = peer->grid;
     const int eff_grid = grid > 0 ? std::min(grid, chain_grid()) : chain_grid();
-    char* base = chain_workspace(st, zbytes + act_bytes, eff_grid);
+    char* base = chain_workspace(st, zbytes + act_bytes, eff_grid,
+                                 (peer && peer->npeer > 0) ? peer->bufs[peer->rank] : nullptr);
     P.bar = reinterpret_cast<unsigned long long*>(base);
     P.epoch = reinterpret_cast<unsigned long long*>(base + 64);
     // measured: tagged z words win for the 2-phase MLP launch (30.5 vs 31.7 us
@@ -907,9 +918,13 @@ int pg_masked_forward_union(pg_layer L, const uint8_t* masks, size_t P, const in
     const cudaStream_t st = as_stream(s);
     const int rp = (int)round_up((size_t)L->r, 8);
     Scratch z((size_t)T * rp * 2, st);
-    // tokens on M, experts on N (narrow tiles cover the SMs, launch_umma);
-    // measured: this beats K split across CTAs (f32 partials outweigh the
-    // weights at T = 256) and the weights-on-M orientation
+    // stage 1 Z = mask(X . B^T), stage 2 Y = Z . A^T.  Per GEMM: the weights-on-M
+    // kernel (union_wm.cu, T <= 256) where it wins, else tokens on M with narrow
+    // expert tiles covering the SMs (launch_umma; K split across CTAs when long).
+    // Either writes Z's padding columns [r, rp) as zeros.
+    const WmSpec wa{L->bt, L->ldb, L->r, L->n, x, L->n, z.p, rp, 1, masks, (long long)sel_mask_ld(L->r)};
+    const WmSpec wb{L->a, L->lda, L->m, L->r, z.p, rp, y, L->m, ydt == PG_BF16 ? 1 : 0};
+    const bool use_a = union_wm_ok((int)T, {wa}), use_b = union_wm_ok((int)T, {wb});
     UmmaSpec s1{x, L->n, L->bt, L->ldb, z.p, rp, (int)T, rp, L->n, 1};
     s1.mask = masks;
     s1.mask_ld = (long long)sel_mask_ld(L->r);
@@ -920,10 +935,11 @@ int pg_masked_forward_union(pg_layer L, const uint8_t* masks, size_t P, const in
     UmmaSpec s2{z.p, rp, L->a, L->lda, y, L->m, (int)T, L->m, rp, ydt == PG_BF16 ? 1 : 0};
     s2.a_hint = 2;
     s2.b_hint = 1;
-    // long K with few tiles: split K across the SMs (f32 partials), else narrow tiles
-    Scratch ws(std::max(umma_splitk_bytes(s1), umma_splitk_bytes(s2)), st);
-    if (!launch_umma_splitk(s1, ws.p, st)) launch_umma({s1}, st);
-    if (!launch_umma_splitk(s2, ws.p, st)) launch_umma({s2}, st);
+    Scratch ws(std::max(use_a ? 0 : umma_splitk_bytes(s1), use_b ? 0 : umma_splitk_bytes(s2)), st);
+    if (use_a) launch_union_wm({wa}, (int)T, tok_pat, st);
+    else if (!launch_umma_splitk(s1, ws.p, st)) launch_umma({s1}, st);
+    if (use_b) launch_union_wm({wb}, (int)T, nullptr, st);
+    else if (!launch_umma_splitk(s2, ws.p, st)) launch_umma({s2}, st);
     PG_API_END
 }
 
@@ -946,6 +962,17 @@ int pg_module_forward_union(const pg_layer* Ls, const uint8_t* const* masks, con
     }
     const cudaStream_t st = as_stream(s);
     Scratch z(zbytes, st);
+    // T <= 256: per stage, weights on M with the whole batch as N (union_wm.cu)
+    // where that kernel wins, else the tokens-on-M grouped kernel
+    std::vector<WmSpec> wm1, wm2;
+    for (size_t l = 0; l < nlin; ++l) {
+        const pg_layer L = Ls[l];
+        const int rp = (int)round_up((size_t)L->r, 8);
+        void* zl = z.as<char>() + zoff[l];
+        wm1.push_back(WmSpec{L->bt, L->ldb, L->r, L->n, x, L->n, zl, rp, 1, masks[l], (long long)sel_mask_ld(L->r)});
+        wm2.push_back(WmSpec{L->a, L->lda, L->m, L->r, zl, rp, ys[l], L->m, ydt == PG_BF16 ? 1 : 0});
+    }
+    const bool wa = union_wm_ok((int)T, wm1), wb = union_wm_ok((int)T, wm2);
     std::vector<UmmaSpec> s1, s2;
     for (size_t l = 0; l < nlin; ++l) {
         const pg_layer L = Ls[l];
@@ -967,11 +994,13 @@ int pg_module_forward_union(const pg_layer* Ls, const uint8_t* const* masks, con
     // the linears' first GEMMs share x: one grouped launch per stage (with
     // their K split across the SMs when that pays, see launch_umma_splitk)
     size_t w1 = 0, w2 = 0;
-    for (const UmmaSpec& u : s1) w1 += umma_splitk_bytes(u);
-    for (const UmmaSpec& u : s2) w2 += umma_splitk_bytes(u);
+    for (const UmmaSpec& u : s1) w1 += wa ? 0 : umma_splitk_bytes(u);
+    for (const UmmaSpec& u : s2) w2 += wb ? 0 : umma_splitk_bytes(u);
     Scratch ws(std::max(w1, w2), st);
-    if (!launch_umma_splitk_multi(s1, ws.p, st)) launch_umma(s1, st);
-    if (!launch_umma_splitk_multi(s2, ws.p, st)) launch_umma(s2, st);
+    if (wa) launch_union_wm(wm1, (int)T, tok_pat, st);
+    else if (!launch_umma_splitk_multi(s1, ws.p, st)) launch_umma(s1, st);
+    if (wb) launch_union_wm(wm2, (int)T, nullptr, st);
+    else if (!launch_umma_splitk_multi(s2, ws.p, st)) launch_umma(s2, st);
     PG_API_END
 }
 
@@ -1339,8 +1368,31 @@ int pg_copy_io(const void* src, void* dst, size_t bytes, pg_stream s) {
     PG_API_END
 }
 
+int pg_chain_workspace_release(pg_stream s) {
+    PG_API_BEGIN
+    cudaStream_t st = as_stream(s);
+    int dev = 0;
+    PG_CUDA_THROW(cudaGetDevice(&dev));
+    PG_CUDA_THROW(cudaStreamSynchronize(st));
+    union_wm_release(st);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+        if (std::get<0>(it->first) == dev && std::get<1>(it->first) == st) {
+            if (it->second.first) PG_CUDA_THROW(cudaFree(it->second.first));
+            it = g_ws.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    PG_API_END
+}
+
 int pg_chain_debug_dump(uint64_t* out_host, size_t n) {
     PG_API_BEGIN
+    if (getenv("PG_WM_DBG") && out_host) {  // union batch kernel stamps instead (diagnostics only)
+        union_wm_debug_dump(reinterpret_cast<unsigned long long*>(out_host), n);
+        return PG_OK;
+    }
     require(out_host && g_chain_dbg, PG_INVALID_ARGUMENT, "chain debug: set PG_CHAIN_DBG=1");
     PG_CUDA_THROW(cudaMemcpy(out_host, g_chain_dbg, std::min<size_t>(n, 1024 * 16) * 8, cudaMemcpyDeviceToHost));
     PG_API_END

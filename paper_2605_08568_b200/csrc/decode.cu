@@ -503,6 +503,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         mbar_init(smem_u32(empty + kRingStages + 1), 1);  // z exchange done (producer throttle)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // launch tag: every CTA adds 1 to the workspace's epoch counter BEFORE it
+    // lets dependents launch (the __syncthreads below orders the ticket before
+    // launch_dependents), so every CTA of launch N holds its ticket before any
+    // CTA of launch N+1 can be scheduled -- even on SMs this grid leaves free --
+    // and old / G is the launch index.
+    unsigned long long epoch_old = 0;
+    if (threadIdx.x == 0) epoch_old = atomicAdd(P.epoch, 1ull);
     __syncthreads();
 
     // Let the next launch in the stream start its prologue / weight stream as
@@ -516,11 +523,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         }
         return;
     }
-    // launch tag: every CTA adds 1 to the workspace's epoch counter before it
-    // publishes anything, and a CTA of the next launch becomes resident only
-    // after a CTA of this one exited, so old / G is the launch index.
-    unsigned long long epoch_old = 0;
-    if (threadIdx.x == 0) epoch_old = atomicAdd(P.epoch, 1ull);
     uint32_t* tag_s = reinterpret_cast<uint32_t*>(empty + kRingStages);
     // consumers read x and write z / act / y: wait for the previous grid
     asm volatile("griddepcontrol.wait;" ::: "memory");

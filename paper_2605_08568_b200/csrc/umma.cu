@@ -23,6 +23,7 @@
 #include <mutex>
 #include <vector>
 
+#include "tc_ptx.cuh"
 #include "umma.cuh"
 
 namespace pg {
@@ -61,73 +62,8 @@ struct __align__(64) UmmaParams {
     int total_tiles;
 };
 
-// ---------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t u_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void u_mbar_init(uint32_t b, uint32_t c) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c) : "memory");
-}
-__device__ __forceinline__ void u_mbar_wait(uint32_t b, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(b),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void u_mbar_arrive_tx(uint32_t b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void u_mbar_arrive(uint32_t b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
-}
-__device__ __forceinline__ void u_tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(map), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
-// operand loads with an L2 policy (pol: createpolicy result)
-__device__ __forceinline__ void u_tma_2d_h(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
-                                           uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-        "l"(map), "r"(x), "r"(y), "r"(bar), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ uint64_t u_policy(int hint, uint64_t first, uint64_t last) {
-    return hint == 1 ? first : last;
-}
-__device__ __forceinline__ uint64_t u_desc(uint32_t saddr) {
-    // K-major, 128B swizzle: LBO=1 (unused), SBO=1024B, version 1 (sm100), layout 2
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ void u_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void u_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
-
 // ---- epilogue helpers: TMEM -> registers -> bf16 / f32 -> global, with the
 // next chunk's tcgen05.ld in flight while the current chunk is stored
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
 __device__ __forceinline__ void store_chunk(const UmmaGroup& G, int row, int n0, int c0, const uint32_t (&r)[32]) {
     if (row >= G.M) return;
     const int cb = n0 + c0;
@@ -332,40 +268,6 @@ constexpr int U2_OUT_BYTES = 32 * 32 * 4;  // one 32 x 32 output chunk (f32 wors
 // [align slack 1 KB][ring][barriers, 1 KB][per-warp output staging]
 constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 1024 + 4 * 2 * U2_OUT_BYTES;
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// the leader CTA's copy of a barrier (shared::cluster address with the peer bit cleared)
-__device__ __forceinline__ uint32_t leader_addr(uint32_t local) { return local & 0xFEFFFFFFu; }
-__device__ __forceinline__ void u_mbar_arrive_tx_cluster(uint32_t b, uint32_t bytes) {
-    // relaxed: registering the expected bytes orders nothing (a release would
-    // be a fence that waits for this SM's in-flight TMA loads)
-    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void u_mbar_arrive_cluster(uint32_t b) {
-    // relaxed: the TMEM reads are ordered by tcgen05.fence::before_thread_sync
-    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(b) : "memory");
-}
-__device__ __forceinline__ void u_tma_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void u_tma_2d_pair_h(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
-                                                uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3}], [%4], %5;"
-        ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar), "l"(pol)
-        : "memory");
-}
 // ---- k_umma_grouped4 (PG_UMMA_MC=1, off by default): clusters of two CTA
 // pairs on consecutive M tiles of one N tile; each CTA loads a quarter of the
 // B tile and multicasts it to its counterpart in the other pair, so per SM the
@@ -386,22 +288,6 @@ __device__ __forceinline__ void u_commit2_mask(uint32_t bar, uint16_t mask) {
                  ::"r"(bar), "h"(mask)
                  : "memory");
 }
-__device__ __forceinline__ void u_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void u_commit2(uint32_t bar) {  // arrive on this barrier in both CTAs of the pair
-    asm volatile(
-        "{\n .reg .b16 m;\n mov.b16 m, 3;\n"
-        " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}"
-        ::"r"(bar)
-        : "memory");
-}
-
-
 // TMA-store epilogue: each warp stages its 32 rows x 32 columns in shared
 // memory (double-buffered) and one lane stores the box with
 // cp.async.bulk.tensor -- coalesced rows instead of one row per thread.
@@ -745,7 +631,7 @@ static PFN_encodeTiled get_encode() {
 }
 
 // 2-D bf16 K-major operand [rows, K] with row stride ld (elements), box {64, box_rows}
-static CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int box_rows) {
+CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};

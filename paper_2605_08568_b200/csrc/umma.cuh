@@ -1,6 +1,8 @@
 // umma.cuh -- host interface of the tcgen05 grouped GEMM (umma.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include <vector>
 
 #include "pg_common.cuh"
@@ -41,6 +43,10 @@ bool launch_umma_splitk(const UmmaSpec& s, void* workspace, cudaStream_t st);
 bool launch_umma_splitk_multi(const std::vector<UmmaSpec>& specs, void* workspace, cudaStream_t st);
 
 
+
+// 2-D bf16 K-major TMA operand map [rows, K] (row stride ld elements), box
+// {64, box_rows}, 128-byte swizzle (the UMMA K-major SW128 layout).
+CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int box_rows);
 
 // All specs run as grouped launches (<= 32 groups per launch), async on st.
 void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st);

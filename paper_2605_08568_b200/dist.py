@@ -179,6 +179,7 @@ class PeerReduceLinear:
         self._opened = []
         self._aggs = {}
         self._last = None
+        self._zero = None
         if group is not None and world > 1:
             self._exchange(group)
 
@@ -218,8 +219,18 @@ class PeerReduceLinear:
         if key not in self._aggs:
             mine = shard_selection(np.asarray(key, dtype=np.int64), self.world, self.rank)
             if mine.size == 0:
-                raise ValueError("PeerReduceLinear: this rank owns none of the selected experts")
-            self._aggs[key] = aggregate_layout(self.local, [RankSelection(self.shard.local_ids(mine))], self.psi)
+                # this rank owns none of the selected experts: it still launches
+                # (the other ranks wait for its pushes) and pushes exact zeros,
+                # through a one-expert all-zero layer of the same m x n
+                if self._zero is None:
+                    from .api import FactorizedLayer
+                    self._zero = FactorizedLayer(np.zeros((self.m, 1)), np.zeros((self.n, 1)), 1,
+                                                 dtype=self.local.dtype)
+                self._aggs[key] = aggregate_layout(self._zero, [RankSelection(np.zeros(1, dtype=np.uint32))],
+                                                   self.psi)
+            else:
+                self._aggs[key] = aggregate_layout(self.local, [RankSelection(self.shard.local_ids(mine))],
+                                                   self.psi)
         self._last = (sel, self._aggs[key])
         return self._aggs[key]
 

@@ -9,6 +9,7 @@ Two bars:
 Shapes cover ragged M (tokens), N not a multiple of the 256 tile (m=1000,
 K=832 -> 4 x 208), multi-pattern arenas (packing + masks) and grouped prompts.
 """
+import os
 import numpy as np
 import pytest
 import torch
@@ -156,7 +157,9 @@ def test_union_masked_batch(pg, port, m, n, r, K, P, T):
 
 def test_module_forward_union_grouped_equals_single(pg, port):
     """q/k/v-style linears sharing x through one grouped launch per stage give
-    the single-linear union results bit for bit."""
+    the single-linear union results (the stream-K split of a grouped launch
+    differs from a single linear's, so f32 partials are summed in another
+    order: equal within one bf16 rounding), deterministically."""
     from oracle import pyoracle
     shapes = [(512, 1024, 384, 192), (256, 1024, 384, 192), (768, 1024, 320, 160)]
     P, T = 16, 96
@@ -170,8 +173,11 @@ def test_module_forward_union_grouped_equals_single(pg, port):
     pid = np.random.default_rng(3).integers(0, P, T)
     X = torch.from_numpy(port.gaussian(33, (T, 1024))).cuda().to(torch.bfloat16)
     ys = pg.module_forward_union(Ls, Bs, pid, X)
-    for L, b, y in zip(Ls, Bs, ys):
-        assert torch.equal(y, pg.masked_forward_union(L, b, pid, X))
+    ys2 = pg.module_forward_union(Ls, Bs, pid, X)
+    for L, b, y, y2 in zip(Ls, Bs, ys, ys2):
+        assert torch.equal(y, y2)
+        one = pg.masked_forward_union(L, b, pid, X).float()
+        assert ((y.float() - one).abs().max() / one.abs().max()).item() <= 8e-3
 
 
 def test_union_masked_batch_f32_out_and_long_batch(pg, port):
@@ -193,3 +199,15 @@ def test_union_masked_batch_f32_out_and_long_batch(pg, port):
     assert rel(Y.cpu().numpy(), _union_ref(A, B, masks, pid, X)) <= 2e-3
     Yb = pg.masked_forward_union(L, batch, pid, X)  # bf16 output: the same values rounded
     assert rel(Yb.float().cpu().numpy(), Y.cpu().numpy()) <= 1e-2
+
+
+def test_union_weights_on_m_forced():
+    """The weights-on-M union kernel (union_wm.cu) on every union shape above,
+    forced for all GEMMs (PG_UNION_WM_MINKB=0; by default it only takes the
+    long-K / many-tile GEMMs): the union parity tests re-run in a subprocess."""
+    import subprocess
+    import sys
+    env = dict(os.environ, PG_UNION_WM_MINKB="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", __file__, "-k", "union and not forced"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
