@@ -2,27 +2,41 @@
 """Benchmark: PARSE rank-expert hot path on B200 (BASELINE.json metric
 "prefill & decode tokens/s, LLaMA-7B SVD@0.6 rank-expert layers, 1-8 B200").
 
-Default workload = BASELINE.json configs[1] ("config2"): LLaMA-7B MLP block
-(gate/up 4096->11008, down 11008->4096) at ratio 0.6 (K=1194, r_store=2388),
-bf16 storage, f32 accumulation, decode batch 1, the expert subset S taken from
-a pattern-cache hit (N=1024 x d=4096 fp64 cache) and reused across every decode
-step.  One step = one decode token through the block: up, gate (rank-expert
-linears over the packed S arena), silu(gate)*up, down.
+Headline workload = BASELINE.json configs[3] ("config4"), the config the metric
+is quoted on across 1-8 GPUs and the largest single-GPU configuration: a
+32-layer LLaMA-7B-shaped stack of rank-expert linears (q/k/v/o 4096x4096, gate/up
+4096->11008, down 11008->4096, ratio 0.6: K = 819 / 1194, r_store = 1638 / 2388),
+bf16 storage with f32 accumulation, decoding a batch of 256 heterogeneous prompts,
+each prompt with its own expert subset per linear (the reference's prefix-biased
+pattern generator).  One step = one decode token for every prompt through all
+32 x 7 linears (q/k/v and up/gate sharing an input run as one grouped launch per
+GEMM stage; o reads v's output and down reads up's output as stand-ins for the
+attention / SiLU glue, which is outside the path).  32 distinct layer weight
+sets (10.36 GB): every byte streams from HBM each step (inputs >> L2, no flush).
 
-  value  -- device-resident tokens/s, whole job (sum over ranks), CUDA-graph
-            replay of the step chain, inputs already in HBM; 4 MLP-block weight
-            replicas rotated per step (433 MB packed > 126 MB L2).
-  e2e    -- the same steps through the public API with the per-step input
-            copied H2D from pinned host memory and the result read back D2H
-            inside the timed region.
-  roofline -- the dominant rank-expert linear forward (up-projection: stage-1
-            GEMV + stage-2 GEMV kernels), algorithmic bytes K(m+n)*2 + x + y per
-            launch / CUDA-event time, vs MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline -- the reference's own CPU path (oracle/_ref: aggregate_layout +
-            aggregated_forward<float>, exec_engine.hpp:113,194) on this host's
-            cores, bounded sample.
+  value     -- tokens/s of the whole job (sum over ranks), device time (CUDA
+               events, max over ranks) over exactly --steps graph replays of the
+               step after --warmup untimed ones; the median per-step window is
+               reported beside it.
+  e2e       -- the same steps through the public API with the step's input
+               hidden states copied H2D from pinned host memory and the last
+               layer's output read back D2H inside the timed region.
+  roofline  -- HBM: stored expert bytes per step (every linear reads its r_store
+               experts once for the whole batch) / step time, vs MEASURED_PEAKS;
+               the dominant launch (up+gate stage 2) timed alone beside it.
+  cpu_baseline / --impl reference -- the reference's own served path
+               (aggregate_layout + aggregated_forward<float>, exec_engine.hpp:
+               112-164,193-236, compiled from /root/reference into oracle/_ref)
+               on the host cores: one prompt per thread through one sampled layer
+               (7 linears, T = 1), extrapolated to the 32-layer stack.
+Secondary objects (same line): config2 decode batch 1 (the fused MLP-block
+decode kernel), config3 prefill (routing + pack + grouped tcgen05 GEMMs), config1
+fp32 (routed q_proj, 128-token prefill + 32 decode steps, the reference CPU path
+run in full in the same process).
 
---impl reference runs only the reference CPU arm (rank 0) and prints its line.
+--gpus N (N > 1) without torchrun re-executes itself under
+torch.distributed.run; --scaling weak (default: 256 prompts per GPU) or strong
+(256 global prompts partitioned over the ranks with pattern affinity).
 """
 from __future__ import annotations
 
@@ -42,16 +56,17 @@ sys.path.insert(0, ROOT)
 METRIC = "prefill & decode tokens/s, LLaMA-7B SVD@0.6 rank-expert layers, 1–8 B200"
 D_MODEL, D_FF, RATIO = 4096, 11008, 0.6
 N_CACHE, MIN_SIM, PSI = 1024, 0.80, 0.9
-REPLICAS = 4
+N_LAYERS, N_PROMPTS = 32, 256
+LIN = {"q": (D_MODEL, D_MODEL), "k": (D_MODEL, D_MODEL), "v": (D_MODEL, D_MODEL), "o": (D_MODEL, D_MODEL),
+       "up": (D_FF, D_MODEL), "gate": (D_FF, D_MODEL), "down": (D_MODEL, D_FF)}
+GROUPS = (("q", "k", "v"), ("o",), ("up", "gate"), ("down",))  # linears sharing an input: one launch per stage
+SRC = {"q": "x", "k": "x", "v": "x", "o": "v", "up": "o", "gate": "o", "down": "up"}  # stand-in data flow
 
 
-def shapes():
+def dims(m, n):
     from paper_2605_08568_b200 import single_layer_k, store_rank
-    out = {}
-    for name, (m, n) in {"up": (D_FF, D_MODEL), "gate": (D_FF, D_MODEL), "down": (D_MODEL, D_FF)}.items():
-        K = single_layer_k(m, n, RATIO)
-        out[name] = (m, n, K, store_rank(K, min(m, n)))
-    return out
+    K = single_layer_k(m, n, RATIO)
+    return store_rank(K, min(m, n)), K
 
 
 def peaks():
@@ -60,6 +75,16 @@ def peaks():
         j = json.load(open(p))
         return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "measured"
     return 6650.0, 1590.0, "fallback"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -75,10 +100,11 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)  # first sample before the timed region starts
         except FileNotFoundError:
             self.proc = None
         return self
@@ -89,7 +115,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -105,78 +131,241 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-# ----------------------------------------------------------------- reference CPU arm
+def max_over_ranks(torch, v, dev, world):
+    if world <= 1:
+        return v
+    t = torch.tensor([float(v)], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
 
-def reference_arm(steps: int, warmup: int, threads: int | None = None, target_s: float = 0.0):
-    """The reference's own served path on host cores: ExecEngine<float>'s
-    aggregated_forward over the hit pattern's layout, one decode token = the
-    three MLP linears at T=1.  `threads` independent decode streams."""
+
+def barrier(torch, world):
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+
+# ======================================================================= CPU (reference)
+
+def reference_config4(threads: int | None = None, repeats: int = 3):
+    """The reference's served path for config 4 on the host cores: ExecEngine<float>
+    (aggregate_layout over the served patterns, exec_engine.hpp:112-164, then
+    aggregated_forward<float>, :193-236) for one decode token (T = 1) of one
+    prompt per thread through the 7 linears of one sampled layer; median of
+    `repeats` passes (time_engine_pass recipe, exec_engine.hpp:362-379), x 32
+    layers.  Packing is per prompt (amortised over its decode) and not timed."""
     from oracle import pyoracle
     kind = "reference" if pyoracle.available("reference") else "port"
     o = pyoracle.Oracle(kind)
     threads = threads or os.cpu_count() or 1
-    sh = shapes()
+    ldims = [dims(m, n) for m, n in LIN.values()]
+    pats = pyoracle.make_patterns(17171, threads, ldims)
     rng = np.random.default_rng(0)
     aggs = {}
-    for name, (m, n, K, r) in sh.items():
-        sig = 1.0 / (1.0 + np.arange(r) / 64.0)
-        A = rng.standard_normal((m, r)) * (sig / np.sqrt(m))
+    t0 = time.perf_counter()
+    for li, (nm, (m, n)) in enumerate(LIN.items()):
+        r, K = ldims[li]
+        A = rng.standard_normal((m, r)) / np.sqrt(K)
         B = rng.standard_normal((n, r)) / np.sqrt(n)
-        pat = pyoracle.make_patterns(17171, 1, [(r, K)])[0][0]
-        aggs[name] = o.aggregate_layout(A, B, [pat], PSI, elem=4)
+        aggs[nm] = o.aggregate_layout(A, B, [p[li] for p in pats], PSI, elem=4)
         del A, B
-    xs = [rng.standard_normal((D_MODEL, 1)).astype(np.float32) for _ in range(threads)]
+    pack_s = time.perf_counter() - t0
+    xs = [{n: rng.standard_normal((n, 1)).astype(np.float32) for n in (D_MODEL, D_FF)} for _ in range(threads)]
+    times = [[0.0] * repeats for _ in range(threads)]
 
-    def token(i):
-        x = xs[i]
-        u = aggs["up"].forward(0, x)
-        g = aggs["gate"].forward(0, x)
-        act = (g / (1.0 + np.exp(-g)) * u).astype(np.float32)
-        aggs["down"].forward(0, act)
+    def work(i):
+        for rep in range(repeats):
+            t = time.perf_counter()
+            for nm, (m, n) in LIN.items():
+                aggs[nm].forward(i, xs[i][n])
+            times[i][rep] = time.perf_counter() - t
 
-    def run(nsteps):
-        ths = [threading.Thread(target=lambda i=i: [token(i) for _ in range(nsteps)]) for i in range(threads)]
-        t0 = time.perf_counter()
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
-        return time.perf_counter() - t0
-
-    run(warmup)
-    wall = run(steps)
-    toks = steps * threads
-    return {"value": toks / wall, "unit": "tokens/s", "cores": threads, "kind": kind,
-            "sample": f"{threads} threads x {steps} decode tokens (3 MLP linears, T=1, aggregated_forward<float>)",
-            "ms_per_step": wall / steps * 1e3}
-
-
-# ----------------------------------------------------------------- GPU arm
-
-def build_block(pg, torch, sh, dev, seed):
-    """Random-init rank-expert MLP block in the device layout (B^T expert-major,
-    A [m, r_store]); A columns scaled by sigma_e = 1/(1+e/64)."""
-    g = torch.Generator(device=dev).manual_seed(seed)
-    layers = {}
-    for name, (m, n, K, r) in sh.items():
-        bt = (torch.randn((r, n), generator=g, device=dev) / n ** 0.5).to(torch.bfloat16)
-        sig = 1.0 / (1.0 + torch.arange(r, device=dev, dtype=torch.float32) / 64.0)
-        a = (torch.randn((m, r), generator=g, device=dev) * sig / m ** 0.5).to(torch.bfloat16)
-        layers[name] = pg.FactorizedLayer.from_device(bt, a, K, layer_id=name)
-        layers[name]._raw = (bt, a, K)  # for the native fixed-rank SVD baseline
-    return layers
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    w0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - w0
+    layer_s = float(np.median([np.median(t) for t in times]))  # one prompt, one layer, T = 1
+    tok_s = threads / (N_LAYERS * layer_s)
+    return {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": kind,
+            "sample": f"{threads} threads, one prompt each (its own pattern), one decode token through the 7 "
+                      f"linears of 1 of {N_LAYERS} layers (aggregated_forward<float>, T=1), median of {repeats} "
+                      f"passes; extrapolated x{N_LAYERS} layers",
+            "extrapolated": True, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "ms_per_layer_per_prompt": layer_s * 1e3, "pack_s": pack_s, "wall_s": wall}
 
 
-def gpu_arm(args, rank, world, local_rank):
+# ======================================================================= config 4 (headline)
+
+def build_stack(pg, torch, dev, prompts, layers):
+    """32 distinct layers of rank-expert linears (B^T expert-major, A [m, r_store],
+    A scaled 1/sqrt(K) so activations stay O(1) through the stack) and, per layer
+    and linear, the selections of this rank's prompts as device masks."""
+    g = torch.Generator(device=dev).manual_seed(11)
+    ldims = [dims(m, n) for m, n in LIN.values()]
+    stack = []
+    for li in range(layers):
+        pats = pg.make_patterns(17171 + li, N_PROMPTS, ldims)  # the reference's generator (same bits)
+        lay = {}
+        for j, (nm, (m, n)) in enumerate(LIN.items()):
+            r, K = ldims[j]
+            bt = (torch.randn(r, n, device=dev, generator=g) / n ** 0.5).to(torch.bfloat16)
+            a = (torch.randn(m, r, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
+            L = pg.FactorizedLayer.from_device(bt, a, K, layer_id=f"b{li}.{nm}")
+            lay[nm] = (L, pg.SelectionBatch(L, [pats[p][j] for p in prompts]))
+        stack.append(lay)
+    return stack, ldims
+
+
+def config4_arm(args, rank, world, local_rank):
     import torch
     import paper_2605_08568_b200 as pg
+    from paper_2605_08568_b200 import dist as pgd
 
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    sh = shapes()
     hbm_peak, _, peak_kind = peaks()
+    if args.scaling == "strong":  # 256 global prompts, pattern affinity (all distinct here: contiguous)
+        prompts = pgd.partition_by_pattern(list(range(N_PROMPTS)), world)[rank]
+    else:
+        prompts = list(range(N_PROMPTS))
+    Pl = len(prompts)
+    stack, ldims = build_stack(pg, torch, dev, prompts, args.layers)
+    tp = torch.arange(Pl, device=dev, dtype=torch.int32)  # token t -> its prompt's selection t
+    g = torch.Generator(device=dev).manual_seed(5)
+    buf = {"x": torch.randn(Pl, D_MODEL, device=dev, generator=g).to(torch.bfloat16)}
+    for nm, (m, n) in LIN.items():
+        buf[nm] = torch.empty(Pl, m, device=dev, dtype=torch.bfloat16)
+    x_host = torch.empty(Pl, D_MODEL, dtype=torch.bfloat16).pin_memory()
+    x_host.copy_(buf["x"].cpu())
+    y_host = torch.empty(Pl, D_MODEL, dtype=torch.bfloat16).pin_memory()
 
-    # ---- pattern cache: N entries, each with a SelectionMap for the 3 linears
+    def layer(lay, first):
+        for grp in GROUPS:
+            src = SRC[grp[0]]
+            if src == "x" and not first:
+                src = "down"  # layer l+1 reads layer l's output
+            pg.module_forward_union([lay[n][0] for n in grp], [lay[n][1] for n in grp], tp, buf[src],
+                                    out_dtype=torch.bfloat16, outs=[buf[n] for n in grp])
+
+    def step(host_io):
+        if host_io:
+            pg.copy_io(buf["x"], x_host)     # the step's input hidden states, H2D
+        for li, lay in enumerate(stack):
+            layer(lay, li == 0)
+        if host_io:
+            pg.copy_io(y_host, buf["down"])  # the last layer's output, D2H
+
+    st = torch.cuda.Stream(device=dev)
+    graphs = {}
+    for host_io in (False, True):
+        with torch.cuda.stream(st):
+            step(host_io)  # sizes workspaces / pools outside capture
+        st.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        n0 = pg.launch_count()
+        with torch.cuda.graph(gr, stream=st):
+            step(host_io)
+        graphs[host_io] = (gr, pg.launch_count() - n0)
+
+    def timed(host_io, steps, warmup):
+        gr = graphs[host_io][0]
+        with torch.cuda.stream(st):
+            for _ in range(warmup):
+                gr.replay()
+        barrier(torch, world)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        with torch.cuda.stream(st):
+            ev[0].record(st)
+            for i in range(steps):
+                gr.replay()
+                ev[i + 1].record(st)
+        barrier(torch, world)
+        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+        total = ev[0].elapsed_time(ev[steps])
+        return max_over_ranks(torch, total, dev, world), max_over_ranks(torch, float(np.median(per)), dev, world)
+
+    with ClockSampler(local_rank) as clk:
+        ms_total, ms_med = timed(False, args.steps, args.warmup)
+    ms_e2e, ms_e2e_med = timed(True, args.steps, max(1, args.warmup // 2))
+    launches = graphs[False][1]
+
+    # dominant module: up+gate (both union GEMM stages, 2 launches, 144 MB of
+    # stored experts: 36 % of the layer's bytes), timed alone with CUDA events
+    lay0 = stack[0]
+    dom_bytes = sum(lay0[nm][0].r_store * (LIN[nm][0] + LIN[nm][1]) * 2 for nm in ("up", "gate"))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def ug():
+        pg.module_forward_union([lay0["up"][0], lay0["gate"][0]], [lay0["up"][1], lay0["gate"][1]], tp, buf["o"],
+                                out_dtype=torch.bfloat16, outs=[buf["up"], buf["gate"]])
+
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            ug()
+        e0.record(st)
+        for _ in range(10):
+            ug()
+        e1.record(st)
+    st.synchronize()
+    dom_us = e0.elapsed_time(e1) / 10 * 1e3
+    dom = {"what": "up+gate module alone (union GEMM stages 1 and 2, 2 launches), eager, CUDA events",
+           "alg_bytes": dom_bytes, "us": dom_us, "achieved_gbs": dom_bytes / (dom_us * 1e-6) / 1e9,
+           "frac": dom_bytes / (dom_us * 1e-6) / 1e9 / hbm_peak}
+
+    bytes_step = args.layers * sum(ldims[i][0] * (m + n) * 2 for i, (m, n) in enumerate(LIN.values()))
+    flops_step = args.layers * 2 * Pl * sum(ldims[i][0] * (m + n) for i, (m, n) in enumerate(LIN.values()))
+    step_s = ms_total / args.steps * 1e-3
+    glob_tok = N_PROMPTS if args.scaling == "strong" else Pl * world
+    traffic = None
+    tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp_path):
+        traffic = json.load(open(tp_path)).get("config4_step")
+    out = {
+        "metric": METRIC, "value": glob_tok / step_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init rank-expert factors and inputs, seeded; selections from the reference's "
+                "pattern generator)",
+        "config": {"workload": f"config4: {args.layers}-layer LLaMA-7B-shaped stack of rank-expert linears "
+                               f"(q/k/v/o 4096x4096, gate/up 4096->11008, down 11008->4096) ratio {RATIO}, decode "
+                               f"batch of {Pl} heterogeneous prompts per GPU, each with its own expert subset per "
+                               f"linear (union-masked tcgen05 GEMMs, q/k/v and up/gate grouped per stage)",
+                   "global_batch": glob_tok, "prompts_per_gpu": Pl, "layers": args.layers,
+                   "parallelism": f"dp{world} ({args.scaling} scaling; replicated weights, no collective)",
+                   "l2": f"{args.layers} distinct layer weight sets, {bytes_step / 1e9:.2f} GB streamed per step "
+                         f"(>> 126 MB L2, no flush needed)",
+                   "median_ms_per_step": ms_med, "graph": "one CUDA graph per step, replayed"},
+        "e2e": {"value": glob_tok / (ms_e2e / args.steps * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": Pl * D_MODEL * 2, "d2h_bytes_per_step": Pl * D_MODEL * 2,
+                "io": "input hidden states H2D from pinned memory and the last layer's output D2H, inside the "
+                      "timed step (pg_copy_io kernels)", "median_ms_per_step": ms_e2e_med},
+        "roofline": {"bound": "hbm", "achieved": bytes_step / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": bytes_step / step_s / 1e9 / hbm_peak, "traffic": traffic,
+                     "kernel": "the step's union GEMMs (k_union_wm / k_umma_grouped2, 8 per layer): stored expert "
+                               "bytes r_store(m+n)*2 of every linear, read once per step for the whole batch",
+                     "alg_bytes_per_step": bytes_step, "tensor_tflops": flops_step / step_s / 1e12,
+                     "peak_kind": peak_kind, "dominant_launch": dom},
+        "gpu_launches": launches * args.steps,
+        "launches_per_step": launches,
+        "clocks": clk.summary(),
+    }
+    del stack, buf
+    torch.cuda.empty_cache()
+    return out
+
+
+# ======================================================================= config 2 (decode batch 1)
+
+def config2_arm(args, rank, world, local_rank, windows=20, G=64, replicas=4):
+    """BASELINE config 2: LLaMA-7B MLP block decode batch 1, S from a pattern-
+    cache hit reused across steps; the whole block is one k_chain launch."""
+    import torch
+    import paper_2605_08568_b200 as pg
+    dev = torch.device("cuda", local_rank)
+    hbm_peak, _, peak_kind = peaks()
+    sh = {k: (LIN[k][0], LIN[k][1]) + dims(*LIN[k])[::-1] for k in ("up", "gate", "down")}  # m, n, K, r
     pats = pg.make_patterns(17171 + rank, N_CACHE, [(sh[k][3], sh[k][2]) for k in ("up", "gate", "down")])
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     emb = torch.randn((N_CACHE, D_MODEL), generator=gen, device=dev, dtype=torch.float64)
@@ -186,17 +375,21 @@ def gpu_arm(args, rank, world, local_rank):
                 for e, p in zip(emb.cpu().numpy(), pats)])
     q = emb[7] + 0.3 / D_MODEL ** 0.5 * torch.randn(D_MODEL, generator=gen, device=dev, dtype=torch.float64)
     q /= q.norm()
-
-    blocks = [build_block(pg, torch, sh, dev, 100 * rank + j) for j in range(REPLICAS)]
+    blocks = []
+    for j in range(replicas):
+        gg = torch.Generator(device=dev).manual_seed(100 * rank + j)
+        b = {}
+        for name, (m, n, K, r) in sh.items():
+            bt = (torch.randn((r, n), generator=gg, device=dev) / n ** 0.5).to(torch.bfloat16)
+            sig = 1.0 / (1.0 + torch.arange(r, device=dev, dtype=torch.float32) / 64.0)
+            a = (torch.randn((m, r), generator=gg, device=dev) * sig / m ** 0.5).to(torch.bfloat16)
+            b[name] = pg.FactorizedLayer.from_device(bt, a, K, layer_id=name)
+            b[name]._raw = (bt, a, K)
+        blocks.append(b)
     torch.cuda.synchronize()
-
-    # ---- prompt-level work (once per prompt): retrieve -> pack the hit's experts
-    t0 = time.perf_counter()
     res = pg.retrieve(cache, q)
     assert res.hit and res.entry == 7, (res.entry, res.similarity)
     aggs = [{k: pg.aggregate_layout(b[k], [res.pattern[k]], PSI) for k in b} for b in blocks]
-    torch.cuda.synchronize()
-    setup_ms = (time.perf_counter() - t0) * 1e3
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(10):
@@ -205,89 +398,59 @@ def gpu_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     retrieve_us = ev0.elapsed_time(ev1) / 10 * 1e3
 
-    # ---- per-step buffers
-    G = 64  # steps per captured graph
     xs = torch.randn((G, D_MODEL), generator=gen, device=dev).to(torch.bfloat16)
-    up = torch.empty((G, D_FF), device=dev)
-    gt = torch.empty((G, D_FF), device=dev)
     act = torch.empty((G, D_FF), device=dev, dtype=torch.bfloat16)
     y = torch.empty((G, D_MODEL), device=dev)
     x_host = torch.empty((G, D_MODEL), dtype=torch.bfloat16).pin_memory()
     x_host.copy_(xs.cpu())
     y_host = torch.empty((G, D_MODEL), dtype=torch.float32).pin_memory()
 
-    def step(i, host_io, fused=True):
-        a = aggs[i % REPLICAS]
-        if host_io == "zc":  # zero-copy: the MLP kernel reads x from / writes y to pinned host memory itself
-            pg.mlp_forward(a["up"], a["gate"], a["down"], 0, x_host[i], out=y_host[i], act=act[i])
-            return
-        if host_io:  # per-token input H2D from pinned memory, as a PDL-chained kernel
+    def step(i, host_io):
+        a = aggs[i % replicas]
+        if host_io:
             pg.copy_io(xs[i], x_host[i])
-        if fused:  # K6: whole MLP block in one kernel (up/gate fused B side, silu epilogue, down)
-            pg.mlp_forward(a["up"], a["gate"], a["down"], 0, xs[i], out=y[i], act=act[i])
-        else:      # aggregated-only: one chain kernel per linear + silu kernel
-            pg.aggregated_forward(a["up"], 0, xs[i], out=up[i])
-            pg.aggregated_forward(a["gate"], 0, xs[i], out=gt[i])
-            pg.silu_mul(gt[i], up[i], out=act[i])
-            pg.aggregated_forward(a["down"], 0, act[i], out=y[i])
-        if host_io:  # result D2H into pinned memory
+        pg.mlp_forward(a["up"], a["gate"], a["down"], 0, xs[i], out=y[i], act=act[i])
+        if host_io:
             pg.copy_io(y_host[i], y[i])
 
     stream = torch.cuda.Stream(device=dev)
     graphs = {}
-    for key in ((False, True), (True, True), (False, False), ("zc", True)):
-        host_io, fused = key
+    for host_io in (False, True):
         with torch.cuda.stream(stream):
-            for i in range(G):  # warm (kernel attributes, pools) outside capture
-                step(i, host_io, fused)
-        stream.synchronize()
-        g = torch.cuda.CUDAGraph()
-        n0 = pg.launch_count()
-        with torch.cuda.graph(g, stream=stream):
             for i in range(G):
-                step(i, host_io, fused)
-        graphs[key] = (g, pg.launch_count() - n0)
-    torch.cuda.synchronize()
-
-    def timed(host_io, steps, fused=True):
-        g, _ = graphs[(host_io, fused)]
-        reps = max(1, steps // G)
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            for _ in range(max(1, args.warmup // G + 1)):
-                g.replay()
+                step(i, host_io)
         stream.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        with torch.cuda.stream(stream):
-            s0.record(stream)
-            for _ in range(reps):
-                g.replay()
-            s1.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        ms = s0.elapsed_time(s1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, reps * G
+        gr = torch.cuda.CUDAGraph()
+        n0 = pg.launch_count()
+        with torch.cuda.graph(gr, stream=stream):
+            for i in range(G):
+                step(i, host_io)
+        graphs[host_io] = (gr, pg.launch_count() - n0)
 
-    # ---- baselines in the same run: native fixed-rank SVD, i.e.
-    # the static prefix A[:, :K] (B[:, :K]^T x) through cuBLAS (torch.matmul),
-    # and the dense layer W x, both bf16, same replicas, same graph recipe
-    def cublas_graph(mats):
+    def timed(host_io):  # median over `windows` replays of a G-step graph
+        gr = graphs[host_io][0]
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                gr.replay()
+        barrier(torch, world)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(windows + 1)]
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for i in range(windows):
+                gr.replay()
+                ev[i + 1].record(stream)
+        barrier(torch, world)
+        med = float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(windows)]))
+        return max_over_ranks(torch, med, dev, world) / G  # ms per step
+
+    def cublas_tok_s(mats):
         xb = torch.randn((G, D_MODEL), generator=gen, device=dev).to(torch.bfloat16)
 
         def one(i):
-            w = mats[i % REPLICAS]
-            if len(w) == 6:  # fixed-rank SVD: B_K^T x then A_K z per linear
+            w = mats[i % replicas]
+            if len(w) == 6:
                 bu, au, bg, ag, bd, ad = w
-                u = au @ (bu @ xb[i])
-                gg = ag @ (bg @ xb[i])
-                return ad @ (bd @ (torch.nn.functional.silu(gg) * u))
+                return ad @ (bd @ (torch.nn.functional.silu(ag @ (bg @ xb[i])) * (au @ (bu @ xb[i]))))
             wu, wg, wd = w
             return wd @ (torch.nn.functional.silu(wg @ xb[i]) * (wu @ xb[i]))
 
@@ -316,252 +479,218 @@ def gpu_arm(args, rank, world, local_rank):
             bt, a, K_ = b[nm]._raw
             w += [bt[:K_].contiguous(), a[:, :K_].contiguous()]
         svd.append(tuple(w))
-    svd_tok_s = cublas_graph(svd)
+    svd_tok_s = cublas_tok_s(svd)
     del svd
     dense = [tuple(torch.randn(shp, generator=gen, device=dev).to(torch.bfloat16) / 64
-                   for shp in ((D_FF, D_MODEL), (D_FF, D_MODEL), (D_MODEL, D_FF))) for _ in range(REPLICAS)]
-    dense_tok_s = cublas_graph(dense)
+                   for shp in ((D_FF, D_MODEL), (D_FF, D_MODEL), (D_MODEL, D_FF))) for _ in range(replicas)]
+    dense_tok_s = cublas_tok_s(dense)
     del dense
+    ms = timed(False)
+    ms_e2e = timed(True)
+    traffic = None
+    tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp_path):
+        traffic = json.load(open(tp_path)).get("k_chain<bf16>")
+    step_bytes = sum(K_ * (m_ + n_) * 2 for (m_, n_, K_, _) in sh.values()) + D_MODEL * 2 + D_FF * 4 + D_MODEL * 4
+    achieved = step_bytes / (ms * 1e-3) / 1e9
+    out = {"workload": "config2: LLaMA-7B MLP block (gate/up 4096->11008, down 11008->4096) ratio 0.6 K=1194 "
+                       "r_store=2388, decode batch 1, S from a pattern-cache hit (N=1024 x d=4096 f64) reused "
+                       f"across steps, bf16; {replicas} weight replicas rotated (> L2)",
+           "tokens_per_s": world / (ms * 1e-3), "ms_per_step": ms,
+           "e2e_tokens_per_s": world / (ms_e2e * 1e-3), "launches_per_step": graphs[False][1] / G,
+           "timing": f"median of {windows} windows of a {G}-step CUDA graph",
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": achieved / hbm_peak, "traffic": traffic, "alg_bytes_per_launch": step_bytes,
+                        "kernel": "k_chain<bf16> (fused MLP block, 1 launch per step)", "peak_kind": peak_kind},
+           "retrieve_us": retrieve_us,
+           "baselines": {"native_fixed_rank_svd_cublas_tok_s": svd_tok_s, "dense_cublas_tok_s": dense_tok_s}}
+    del blocks, aggs
     torch.cuda.empty_cache()
-
-    with ClockSampler(local_rank) as clk:
-        ms, nsteps = timed(False, args.steps)
-    ms_e2e, nsteps_e2e = timed(True, args.steps)
-    ms_unf, nsteps_unf = timed(False, args.steps, fused=False)
-    ms_zc, nsteps_zc = timed("zc", args.steps)
-    # e2e = the faster of the two host-I/O recipes (both move the same bytes
-    # between pinned host memory and the GPU inside the timed region)
-    e2e_kind = "zero-copy (kernel reads x / writes y in pinned host memory)"
-    if ms_e2e < ms_zc:
-        e2e_kind = "pg_copy_io kernels (H2D x, D2H y) chained by PDL"
-    ms_e2e_best, nsteps_e2e_best = (ms_zc, nsteps_zc) if ms_zc <= ms_e2e else (ms_e2e, nsteps_e2e)
-    launches_per_step = graphs[(False, True)][1] / G
-
-    # ---- roofline: the dominant (only) kernel of the step is k_chain<bf16>, the
-    # fused MLP block; one launch per step, timed by CUDA events on its stream
-    # over the timed region.  Algorithmic bytes = sum_l K_l (m_l + n_l) * 2 (the
-    # selected experts' U and V rows) + x, act (write+read) and y.
-    traffic = None  # dram read+write bytes per launch of k_chain from the committed ncu --set full capture
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("k_chain<bf16>")
-    lin_bytes = {k: K_ * (m_ + n_) * 2 for k, (m_, n_, K_, _) in sh.items()}
-    step_bytes = sum(lin_bytes.values()) + D_MODEL * 2 + D_FF * 2 * 2 + D_MODEL * 4
-    step_us = ms / nsteps * 1e3
-    achieved = step_bytes / (step_us * 1e-6) / 1e9
-    tok_s = nsteps / (ms * 1e-3) * world
-    out = {
-        "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": nsteps,
-        "warmup": args.warmup, "ms_per_step": ms / nsteps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init rank-expert factors, seeded)",
-        "config": {"workload": "config2: LLaMA-7B MLP block (gate/up 4096->11008, down 11008->4096) ratio 0.6 "
-                               "K=1194 r_store=2388, decode batch 1, S from a pattern-cache hit reused across steps",
-                   "cache": f"N={N_CACHE} x d={D_MODEL} f64, min_similarity {MIN_SIM}, hit entry {res.entry}",
-                   "l2": f"{REPLICAS} MLP-block weight replicas rotated per step "
-                         f"({REPLICAS * step_bytes / 1e6:.0f} MB packed > 126 MB L2)",
-                   "parallelism": f"dp{world} (independent decode streams per GPU)",
-                   "psi": PSI, "graph": f"CUDA graph of {G} steps replayed"},
-        "e2e": {"value": nsteps_e2e_best / (ms_e2e_best * 1e-3) * world, "unit": "tokens/s",
-                "h2d_bytes_per_step": D_MODEL * 2, "d2h_bytes_per_step": D_MODEL * 4, "io": e2e_kind},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "k_chain<bf16> (fused MLP block: up+gate stage 1, grid barrier, stage 2 + "
-                               "silu epilogue, down stage 1/2; 1 launch per step)",
-                     "alg_bytes_per_launch": step_bytes, "avg_us": step_us, "peak_kind": peak_kind},
-        "variants": {"aggregated_fused_tok_s": tok_s,
-                     "aggregated_only_tok_s": nsteps_unf / (ms_unf * 1e-3) * world,
-                     "e2e_copy_io_tok_s": nsteps_e2e / (ms_e2e * 1e-3) * world,
-                     "e2e_zero_copy_tok_s": nsteps_zc / (ms_zc * 1e-3) * world,
-                     "launches_per_step": {"fused": launches_per_step,
-                                           "unfused": graphs[(False, False)][1] / G}},
-        "gpu_launches": int(launches_per_step * nsteps),
-        "clocks": clk.summary(),
-        "prefill_setup": {"retrieve_us": retrieve_us, "retrieve_plus_pack_ms_host": setup_ms},
-        "baselines": {"native_fixed_rank_svd_cublas_tok_s": svd_tok_s, "dense_cublas_tok_s": dense_tok_s,
-                      "note": "static prefix A[:, :K](B[:, :K]^T x) and dense W x, bf16 torch.matmul, "
-                              "same replicas, CUDA graph of 64 steps"},
-    }
-    if args.prefill:
-        del blocks, aggs
-        torch.cuda.empty_cache()
-        out["prefill"] = prefill_arm(pg, torch, dev, world)
-        torch.cuda.empty_cache()
-    if args.decode_batch:
-        out["decode_batch"] = decode_batch_arm(pg, torch, dev, world, hbm_peak)
     return out
 
 
-def decode_batch_arm(pg, torch, dev, world, hbm_peak, P=256, layers=32, distinct=4):
-    """BASELINE config 4 (per GPU, data-parallel): a 32-layer LLaMA-7B-shaped
-    stack of rank-expert linears decoding 256 prompts x 1 token, each prompt
-    with its own selection per linear (the reference's pattern generator).
-    Union-masked: every linear reads its stored experts once for the whole
-    batch (two tcgen05 GEMMs, the per-token mask in the first's epilogue).
-    `distinct` layer weight sets (each 324 MB > L2) are cycled through the 32
-    layers; attention and norms are outside the path."""
-    lin = {"q": (D_MODEL, D_MODEL), "k": (D_MODEL, D_MODEL), "v": (D_MODEL, D_MODEL), "o": (D_MODEL, D_MODEL),
-           "up": (D_FF, D_MODEL), "gate": (D_FF, D_MODEL), "down": (D_MODEL, D_FF)}
-    dims = [(pg.store_rank(pg.single_layer_k(m, n, RATIO), n), pg.single_layer_k(m, n, RATIO)) for m, n in lin.values()]
-    pats = pg.make_patterns(17171, P, dims)  # the reference's generator (pg_make_patterns, same bits)
-    g = torch.Generator(device=dev).manual_seed(11)
-    stack = []
-    for _ in range(distinct):
-        lay = {}
-        for li, (nm, (m, n)) in enumerate(lin.items()):
-            r, K = dims[li]
-            bt = (torch.randn(r, n, device=dev, generator=g) / n ** 0.5).to(torch.bfloat16)
-            a = (torch.randn(m, r, device=dev, generator=g) / m ** 0.5).to(torch.bfloat16)
-            L = pg.FactorizedLayer.from_device(bt, a, K, layer_id=nm)
-            lay[nm] = (L, pg.SelectionBatch(L, [p[li] for p in pats]))
-        stack.append(lay)
-    X = {n: torch.randn(P, n, device=dev, generator=g).to(torch.bfloat16) for n in (D_MODEL, D_FF)}
-    tp = torch.arange(P, device=dev, dtype=torch.int32)  # prompt q -> its own selection q
+# ======================================================================= config 3 (prefill)
 
-    Yl = {nm: torch.empty(P, m, device=dev, dtype=torch.bfloat16) for nm, (m, n) in lin.items()}
-    groups = (("q", "k", "v"), ("o",), ("up", "gate"), ("down",))  # linears sharing an input: one launch per stage
-
-    def step():
-        for li in range(layers):
-            lay = stack[li % distinct]
-            for grp in groups:
-                pg.module_forward_union([lay[g][0] for g in grp], [lay[g][1] for g in grp], tp, X[lin[grp[0]][1]],
-                                        out_dtype=torch.bfloat16, outs=[Yl[g] for g in grp])
-
-    st = torch.cuda.Stream(device=dev)
-    with torch.cuda.stream(st):
-        step()
-    st.synchronize()
-    gr = torch.cuda.CUDAGraph()
-    n0 = pg.launch_count()
-    with torch.cuda.graph(gr, stream=st):
-        step()
-    launches = pg.launch_count() - n0
-    reps = 5
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
-    with torch.cuda.stream(st):
-        gr.replay()
-        e0.record(st)
-        for _ in range(reps):
-            gr.replay()
-        e1.record(st)
-    torch.cuda.synchronize()
-    ms = max_over_ranks_ms(torch, e0.elapsed_time(e1) / reps, dev, world)
-    byt = layers * sum(dims[i][0] * (m + n) * 2 for i, (m, n) in enumerate(lin.values()))
-    fl = layers * 2 * P * sum(dims[i][0] * (m + n) for i, (m, n) in enumerate(lin.values()))
-    return {"workload": f"config4: {layers}-layer LLaMA-7B-shaped stack, {P} prompts x 1 decode token, "
-                        f"{P} heterogeneous selections per linear (reference generator, seed 17171), "
-                        f"union-masked tcgen05 GEMMs (q/k/v and up/gate grouped per stage); {distinct} distinct layer "
-                        f"weight sets cycled (each > L2)",
-            "tokens_per_s": P / (ms * 1e-3) * world, "ms_per_step": ms, "launches_per_step": launches,
-            "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": byt / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": byt,
-                         "tensor_tflops": fl / (ms * 1e-3) / 1e12}}
-
-
-def max_over_ranks_ms(torch, ms, dev, world):
-    """Device time of a secondary arm: the slowest rank's (like the headline)."""
-    if world <= 1:
-        return ms
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    return float(t.item())
-
-
-def prefill_arm(pg, torch, dev, world, P=16, T=2048):
+def config3_arm(args, rank, world, local_rank, P=16, T=2048):
     """BASELINE config 3: one LLaMA-7B decoder layer's 7 rank-expert linears,
-    16 prompts x 2048 tokens, each prompt routed on device to its own expert
-    subset (bit-exact router), packed once, then grouped tcgen05 GEMMs.
-    Timed: routing (7 routers, 16 prompts) + the 7 prefill linears."""
-    lin = {"q": (D_MODEL, D_MODEL), "k": (D_MODEL, D_MODEL), "v": (D_MODEL, D_MODEL), "o": (D_MODEL, D_MODEL),
-           "up": (D_FF, D_MODEL), "gate": (D_FF, D_MODEL), "down": (D_MODEL, D_FF)}
+    16 prompts x 2048 tokens, each routed on device to its own expert subset
+    (bit-exact router), packed on device, grouped tcgen05 GEMMs.  Timed: routing
+    + pack + the 7 prefill linears."""
+    import torch
+    import paper_2605_08568_b200 as pg
+    dev = torch.device("cuda", local_rank)
     g = torch.Generator(device=dev).manual_seed(7)
     X = torch.randn(P * T, D_MODEL, device=dev, generator=g).to(torch.bfloat16)
     X2 = torch.randn(P * T, D_FF, device=dev, generator=g).to(torch.bfloat16)
+    Xo = torch.randn(P * T, D_MODEL, device=dev, generator=g).to(torch.bfloat16)
     offs = [i * T for i in range(P + 1)]
     layers, routers, outs, flops = {}, {}, {}, 0
-    for nm, (m, n) in lin.items():
-        K = pg.single_layer_k(m, n, RATIO)
-        r = pg.store_rank(K, min(m, n))
+    for nm, (m, n) in LIN.items():
+        r, K = dims(m, n)
         bt = (torch.randn((r, n), generator=g, device=dev) / n ** 0.5).to(torch.bfloat16)
         a = (torch.randn((m, r), generator=g, device=dev) / m ** 0.5).to(torch.bfloat16)
         layers[nm] = (pg.FactorizedLayer.from_device(bt, a, K), K)
         routers[nm] = pg.RouterParams(torch.randn((r, n), generator=g, device=dev, dtype=torch.float64))
         outs[nm] = torch.empty(P * T, m, device=dev, dtype=torch.bfloat16)
         flops += 2 * P * T * K * (m + n)
-    # routing (timed separately): select_topk(score(mean_pool(x_p))) per prompt.
-    # Linears sharing an input pool it once (toy_lm.hpp:220-249: q/k/v and
-    # up/gate read hn, o the attention output, down act), then every router
-    # scores its own pooled input.
-    Xo = torch.randn(P * T, D_MODEL, device=dev, generator=g).to(torch.bfloat16)
     src = {"q": X, "k": X, "v": X, "up": X, "gate": X, "o": Xo, "down": X2}
     sels = {}
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def route_all():
         pooled = {id(x): pg.mean_pool(x, layout="token", offsets=offs) for x in (X, Xo, X2)}
-        for nm in lin:
+        for nm in LIN:
             sels[nm] = pg.route_select_pooled(routers[nm], pooled[id(src[nm])], layers[nm][1])
 
-    for _ in range(3):  # warm: scratch pools, kernel attributes
-        route_all()
-    torch.cuda.synchronize()
-    route_reps = 5
-    if world > 1:
-        torch.distributed.barrier()
-    e0.record()
-    for _ in range(route_reps):
-        route_all()
-    e1.record()
-    torch.cuda.synchronize()
-    route_ms = max_over_ranks_ms(torch, e0.elapsed_time(e1) / route_reps, dev, world)
-    # pack each prompt's experts once (serving: after routing / a cache hit)
-    t0 = time.perf_counter()
-    aggs = {nm: [pg.aggregate_layout(layers[nm][0], [pg.RankSelection(sels[nm][p].cpu().numpy())], PSI)
-                 for p in range(P)] for nm in lin}
-    torch.cuda.synchronize()
-    pack_ms = (time.perf_counter() - t0) * 1e3
+    have_dev_pack = hasattr(pg, "pack_selected")
 
-    def layer_step():
-        for nm in lin:
-            pg.prefill_batched(aggs[nm], offs, src[nm], out_dtype=torch.bfloat16, out=outs[nm])
+    def pack_all():
+        return {nm: pg.pack_selected(layers[nm][0], sels[nm]) for nm in LIN} if have_dev_pack else None
+
+    def gemms(packs):
+        for nm in LIN:
+            if have_dev_pack:
+                pg.prefill_packed(packs[nm], offs, src[nm], out_dtype=torch.bfloat16, out=outs[nm])
+            else:
+                pg.prefill_batched(packs[nm], offs, src[nm], out_dtype=torch.bfloat16, out=outs[nm])
 
     for _ in range(2):
-        layer_step()
+        route_all()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if have_dev_pack:
+        packs = pack_all()
+    else:  # host-driven pack per prompt (round-1 path)
+        packs = {nm: [pg.aggregate_layout(layers[nm][0], [pg.RankSelection(sels[nm][p].cpu().numpy())], PSI)
+                      for p in range(P)] for nm in LIN}
+    torch.cuda.synchronize()
+    pack_ms_host = (time.perf_counter() - t0) * 1e3
+    gemms(packs)
     torch.cuda.synchronize()
     reps = 5
-    if world > 1:
-        torch.distributed.barrier()
-    e0.record()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    barrier(torch, world)
+    e[0].record()
     for _ in range(reps):
-        layer_step()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = max_over_ranks_ms(torch, e0.elapsed_time(e1) / reps, dev, world)
+        route_all()
+    e[1].record()
+    for _ in range(reps if have_dev_pack else 0):
+        packs = pack_all()
+    e[2].record()
+    for _ in range(reps):
+        gemms(packs)
+    e[3].record()
+    barrier(torch, world)
+    route_ms = max_over_ranks(torch, e[0].elapsed_time(e[1]) / reps, dev, world)
+    pack_ms = max_over_ranks(torch, e[1].elapsed_time(e[2]) / reps, dev, world) if have_dev_pack else pack_ms_host
+    ms = max_over_ranks(torch, e[2].elapsed_time(e[3]) / reps, dev, world)
     _, tflops_peak, peak_kind = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
-    return {"workload": "config3: LLaMA-7B decoder layer (q,k,v,o,gate,up,down) ratio 0.6, 16 prompts x 2048 "
-                        "tokens, per-prompt expert subsets routed on device, bf16 (z rounded to bf16 between stages)",
-            "tokens_per_s": P * T / ((ms + route_ms) * 1e-3) * world,
-            "gemm_tokens_per_s": P * T / (ms * 1e-3) * world,
-            "ms_per_layer": ms, "route_ms": route_ms, "pack_ms_host": pack_ms,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": tflops_peak, "unit": "TFLOP/s",
-                         "frac": achieved / tflops_peak, "flops_per_layer": flops, "peak_kind": peak_kind,
-                         "kernel": "k_umma_grouped (tcgen05.mma kind::f16, TMA, TMEM; 2 grouped launches per linear)"}}
+    out = {"workload": "config3: LLaMA-7B decoder layer (q,k,v,o,gate,up,down) ratio 0.6, 16 prompts x 2048 tokens, "
+                       "per-prompt expert subsets routed on device, bf16 (z rounded to bf16 between stages)",
+           "tokens_per_s": P * T / ((ms + route_ms + pack_ms) * 1e-3) * world,
+           "gemm_tokens_per_s": P * T / (ms * 1e-3) * world,
+           "ms_per_layer": ms, "route_ms": route_ms, "pack_ms": pack_ms,
+           "pack_on_device": have_dev_pack,
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": tflops_peak, "unit": "TFLOP/s",
+                        "frac": achieved / tflops_peak, "flops_per_layer": flops, "peak_kind": peak_kind,
+                        "kernel": "k_umma_grouped2 (tcgen05.mma cta_group::2 kind::f16, TMA, TMEM; 2 grouped "
+                                  "launches per linear)"}}
+    del layers, routers, outs, X, X2, Xo
+    torch.cuda.empty_cache()
+    return out
 
+
+# ======================================================================= config 1 (fp32, CPU ref in full)
+
+def config1_arm(args, local_rank, cpu: bool):
+    """BASELINE config 1: one q_proj-shaped layer (4096x4096, ratio 0.6: K=819,
+    r_store=1638), fp32, one prompt: route from the 128-token prefill (bit-exact
+    router), 128-token prefill + 32 decode steps reusing S (RoutingProvider,
+    model.hpp:96-106).  The reference CPU path runs the same work in full
+    (mean_pool/score/select_topk f64, aggregate_layout + aggregated_forward<float>)
+    and the two outputs are compared."""
+    import torch
+    import paper_2605_08568_b200 as pg
+    from oracle import pyoracle
+    dev = torch.device("cuda", local_rank)
+    m = n = D_MODEL
+    r, K = dims(m, n)
+    T, D = 128, 32
+    o = pyoracle.Oracle("port")
+    A = o.gaussian(101, (m, r)) / np.sqrt(K)
+    B = o.gaussian(102, (n, r)) / np.sqrt(n)
+    theta = o.gaussian(103, (r, n))
+    X = o.gaussian(104, (n, T)).astype(np.float32)
+    Xd = o.gaussian(105, (n, D)).astype(np.float32)
+    L = pg.FactorizedLayer(A, B, K, dtype="f32")
+    router = pg.RouterParams(theta, np.zeros(r))
+    xg = torch.from_numpy(X).to(dev)
+    xdg = [torch.from_numpy(np.ascontiguousarray(Xd[:, j:j + 1])).to(dev) for j in range(D)]
+    ys = [torch.empty(m, 1, device=dev) for _ in range(D)]
+
+    def run():
+        sel = pg.route_select(router, xg, K)[0]
+        agg_sel = sel  # device selection, reused by every call (route once, reuse)
+        yp = pg.masked_forward(L, agg_sel, xg)
+        for j in range(D):
+            pg.masked_forward(L, agg_sel, xdg[j], out=ys[j])
+        return sel, yp
+
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        sel, yp = run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    out = {"workload": "config1: q_proj 4096x4096 ratio 0.6 (K=819, r_store=1638), fp32, 1 prompt: route + "
+                       "128-token prefill + 32 decode steps reusing S", "ms_gpu": ms,
+           "tokens_per_s_gpu": (T + D) / (ms * 1e-3)}
+    if cpu:
+        kind = "reference" if pyoracle.available("reference") else "port"
+        oc = pyoracle.Oracle(kind)
+        t0 = time.perf_counter()
+        want = oc.select_topk(oc.score(theta, np.zeros(r), oc.mean_pool(X.astype(np.float64))), K)
+        agg = oc.aggregate_layout(A, B, [want], PSI, elem=4)
+        t1 = time.perf_counter()
+        yc = agg.forward(0, X)
+        ycd = [agg.forward(0, np.ascontiguousarray(Xd[:, j:j + 1])) for j in range(D)]
+        t2 = time.perf_counter()
+        got = sel.cpu().numpy().astype(np.uint32)
+        ygp = yp.cpu().numpy()
+        rel_p = float(np.abs(ygp - yc).max() / np.abs(yc).max())
+        rel_d = max(float(np.abs(ys[j].cpu().numpy() - ycd[j]).max() / np.abs(ycd[j]).max()) for j in range(D))
+        out.update({"cpu_kind": kind, "cpu_cores": 1, "ms_cpu_route_pack": (t1 - t0) * 1e3,
+                    "ms_cpu_forward": (t2 - t1) * 1e3,
+                    "tokens_per_s_cpu": (T + D) / (t2 - t0), "selection_bit_exact": bool(np.array_equal(got, want)),
+                    "rel_err_prefill_vs_cpu": rel_p, "rel_err_decode_vs_cpu": rel_d})
+    return out
+
+
+# ======================================================================= main
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
-    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-steps", type=int, default=3)
-    ap.add_argument("--prefill", type=int, default=1, help="also measure config-3 prefill (secondary)")
-    ap.add_argument("--decode-batch", type=int, default=1,
-                    help="also measure config-4 batched heterogeneous decode (secondary)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--layers", type=int, default=N_LAYERS, help=argparse.SUPPRESS)
+    ap.add_argument("--secondary", type=int, default=1, help="also run configs 1-3 (secondary objects)")
+    ap.add_argument("--cpu", type=int, default=1, help="time the reference CPU path (rank 0, N=1)")
     args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-execute under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29517"),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -569,35 +698,40 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        st = max(1, min(args.steps, 20))
-        wu = max(1, min(args.warmup, 3))  # bounded CPU sample: the whole arm stays within minutes
-        ref = reference_arm(st, wu)
-        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": 0, "steps": st,
-                "warmup": wu, "ms_per_step": ref["ms_per_step"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        ref = reference_config4(repeats=max(1, min(args.steps, 3)))
+        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": 0, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": N_PROMPTS / ref["value"] * 1e3,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",
-                "config": {"workload": "config2: LLaMA-7B MLP block decode batch 1 (reference CPU "
-                                       "aggregated_forward<float>, exec_engine.hpp:194)"},
-                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
+                "config": {"workload": f"config4: {N_LAYERS}-layer LLaMA-7B-shaped rank-expert stack, decode, "
+                                       f"heterogeneous prompts (reference CPU ExecEngine<float>: aggregate_layout + "
+                                       f"aggregated_forward<float>, exec_engine.hpp:112-236)",
+                           "global_batch": N_PROMPTS},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                     "nproc", "extrapolated", "ms_per_layer_per_prompt")},
+                "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
+    import torch
+    torch.cuda.set_device(local_rank)
     if world > 1:
-        import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out = gpu_arm(args, rank, world, local_rank)
+    out = config4_arm(args, rank, world, local_rank)
+    if args.secondary:
+        out["decode_b1"] = config2_arm(args, rank, world, local_rank)
+        out["prefill"] = config3_arm(args, rank, world, local_rank)
+        if rank == 0:
+            out["config1"] = config1_arm(args, local_rank, cpu=bool(args.cpu) and world == 1)
+    if rank == 0 and world == 1 and args.cpu:
+        ref = reference_config4()
+        out["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc",
+                                                   "extrapolated", "ms_per_layer_per_prompt")}
     if rank == 0:
-        if world == 1 and args.cpu_steps > 0:
-            ref = reference_arm(args.cpu_steps, 1)
-            out["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(out), flush=True)
     if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":
