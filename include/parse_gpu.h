@@ -265,6 +265,22 @@ int pg_ipc_close(void* dev_ptr);
 int pg_prefill_batched(const pg_agg* aggs, const int64_t* offsets_host, size_t n_prompts,
                        const void* x_dev, void* y_dev, pg_dtype y_dtype, pg_stream stream);
 
+/* Routed prefill with the expert pack on device (config 3; exec_engine.hpp:
+ * 112-164's column copies for one pattern per prompt, then
+ * aggregated_forward<T> :193-236 as tcgen05 GEMMs).  sel_dev [P, k] int32 holds
+ * every prompt's K ascending expert ids on the device (pg_route_select /
+ * pg_route_select_pooled output: no host round trip).  pg_pack_selected packs
+ * them into caller buffers bt_out [P][kp][ldb] and a_out [P][m][kp] (kp = k
+ * rounded up to 8, zero padded; sizes from pg_pack_bytes); pg_prefill_packed
+ * runs prompt p (tokens offsets_host[p]:offsets_host[p+1] of token-major x)
+ * through its packed experts.  bf16 layers; asynchronous on `stream`. */
+int pg_pack_bytes(pg_layer layer, size_t k, size_t n_prompts, size_t* bt_bytes, size_t* a_bytes);
+int pg_pack_selected(pg_layer layer, const int32_t* sel_dev, size_t k, size_t n_prompts, void* bt_out,
+                     void* a_out, pg_stream stream);
+int pg_prefill_packed(pg_layer layer, const void* bt_packed, const void* a_packed, size_t k,
+                      const int64_t* offsets_host, size_t n_prompts, const void* x_dev, void* y_dev,
+                      pg_dtype y_dtype, pg_stream stream);
+
 /* K5 primitive: C[M, N] = A[M, K] . B[N, K]^T on the tcgen05 tensor cores
  * (bf16 operands, both K-major with 16-byte aligned rows, f32 accumulation;
  * out bf16 when out_bf16 else f32).  The prefill paths are two of these per

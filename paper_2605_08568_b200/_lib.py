@@ -91,6 +91,9 @@ _SIGS = {
     "pg_gemm_bf16": [_vp, C.c_int64, _vp, C.c_int64, _vp, C.c_int64, _sz, _sz, _sz, _i, _vp],
     "pg_chain_debug_dump": [C.POINTER(C.c_uint64), _sz],
     "pg_chain_workspace_release": [_vp],
+    "pg_pack_bytes": [_vp, _sz, _sz, _sp, _sp],
+    "pg_pack_selected": [_vp, _vp, _sz, _sz, _vp, _vp, _vp],
+    "pg_prefill_packed": [_vp, _vp, _vp, _sz, _i64p, _sz, _vp, _vp, _i, _vp],
     "pg_mlp_forward": [_vp, _vp, _vp, _sp, _vp, _vp, _vp, _vp, _i, _vp],
 }
 _VOID = {

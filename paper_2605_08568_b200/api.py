@@ -640,6 +640,49 @@ def prefill_batched(aggs: list, offsets, x: torch.Tensor, out_dtype=None, out: t
     return y
 
 
+class PackedExperts:
+    """Every prompt's selected experts packed on device (K3 for a routed batch,
+    exec_engine.hpp:112-164 with one pattern per prompt): B^T rows [P, kp, ldb]
+    and A columns [P, m, kp] in caller-owned (torch) buffers."""
+
+    def __init__(self, layer: FactorizedLayer, k: int, n_prompts: int, bt: torch.Tensor, a: torch.Tensor):
+        self.layer, self.k, self.P, self.bt, self.a = layer, k, n_prompts, bt, a
+
+
+def pack_selected(layer: FactorizedLayer, sel: torch.Tensor) -> PackedExperts:
+    """Pack each prompt's selection sel [P, K] (device int32, ascending; the
+    router's output) on the device -- no host round trip, no synchronisation."""
+    if not (isinstance(sel, torch.Tensor) and sel.is_cuda):
+        raise ValueError("pack_selected: device selection tensor [P, K] expected")
+    if sel.dim() == 1:
+        sel = sel.unsqueeze(0)
+    sel = sel.to(torch.int32).contiguous()
+    P, k = sel.shape
+    bb, ab = C.c_size_t(), C.c_size_t()
+    call("pg_pack_bytes", layer.handle, k, P, C.byref(bb), C.byref(ab))
+    bt = torch.empty(bb.value, dtype=torch.uint8, device=sel.device)
+    a = torch.empty(ab.value, dtype=torch.uint8, device=sel.device)
+    call("pg_pack_selected", layer.handle, _ptr(sel), k, P, _ptr(bt), _ptr(a), _stream())
+    return PackedExperts(layer, k, P, bt, a)
+
+
+def prefill_packed(packed: PackedExperts, offsets, x: torch.Tensor, out_dtype=None,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+    """Routed heterogeneous prefill (config 3): prompt p (tokens
+    offsets[p]:offsets[p+1] of token-major x [T, n]) through its packed experts,
+    as grouped tcgen05 GEMMs."""
+    L = packed.layer
+    x = _dev(x, torch.bfloat16)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    if offs.size != packed.P + 1 or x.dim() != 2 or x.shape[1] != L.n or offs[-1] > x.shape[0]:
+        raise ValueError("prefill_packed: bad X shape / offsets")
+    ydt = _out_dtype(L.dtype, out_dtype)
+    y = out if out is not None else torch.empty((x.shape[0], L.m), dtype=_TORCH[ydt], device=x.device)
+    call("pg_prefill_packed", L.handle, _ptr(packed.bt), _ptr(packed.a), packed.k,
+         offs.ctypes.data_as(C.POINTER(C.c_int64)), packed.P, _ptr(x), _ptr(y), ydt, _stream())
+    return y
+
+
 def scattered_forward(layer: FactorizedLayer, sel, x: torch.Tensor, trace: AccessTrace | None = None,
                       layout: str = "feature", out_dtype=None) -> torch.Tensor:
     """exec_engine.hpp:239-252: K strided column gathers in S order."""

@@ -44,6 +44,8 @@ void launch_embed_finish(double* h, int d, int* flag, cudaStream_t st);
 int max_cache_dim();
 void launch_gather_rows(pg_dtype dt, const void* src, int64_t lds, const int32_t* idx, int cnt,
                         int cnt_pad, int cols, void* dst, int64_t ldd, cudaStream_t st);
+void launch_pack_selected(const void* bt, int64_t ldb, const void* a, int64_t lda, int r, int n, int m,
+                          const int32_t* sel, int k, int P, void* bt_out, void* a_out, cudaStream_t st);
 void launch_gather_cols(pg_dtype dt, const void* src, int64_t lds, const int32_t* idx, int cnt,
                         int cnt_pad, int m, void* dst, int64_t ldd, cudaStream_t st);
 int decode_tmax(int T);
@@ -1414,6 +1416,69 @@ extern "C" int pg_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t l
     require(a && b && out, PG_INVALID_ARGUMENT, "gemm: null operand");
     require(K % 8 == 0 && lda % 8 == 0 && ldb % 8 == 0, PG_INVALID_ARGUMENT, "gemm: rows must be 16-byte aligned");
     launch_umma({UmmaSpec{a, lda, b, ldb, out, ldo, (int)M, (int)N, (int)K, out_bf16}}, as_stream(s));
+    PG_API_END
+}
+
+// ------------------------------------------------------------ routed prefill (device pack)
+extern "C" int pg_pack_bytes(pg_layer L, size_t k, size_t n_prompts, size_t* bt_bytes, size_t* a_bytes) {
+    PG_API_BEGIN
+    require(L && bt_bytes && a_bytes && k >= 1 && k <= (size_t)L->r, PG_INVALID_ARGUMENT, "pack_bytes: bad arguments");
+    const size_t kp = round_up(k, 8), es = dtype_size(L->dt);
+    *bt_bytes = n_prompts * kp * (size_t)L->ldb * es;
+    *a_bytes = n_prompts * (size_t)L->m * kp * es;
+    PG_API_END
+}
+
+extern "C" int pg_pack_selected(pg_layer L, const int32_t* sel_dev, size_t k, size_t P, void* bt_out, void* a_out,
+                                pg_stream s) {
+    PG_API_BEGIN
+    require(L && sel_dev && bt_out && a_out && P > 0, PG_INVALID_ARGUMENT, "pack_selected: bad arguments");
+    require(L->dt == PG_BF16, PG_INVALID_ARGUMENT, "pack_selected: bf16 layers (tensor-core prefill path)");
+    if (k == 0 || k > (size_t)L->r) throw Error{PG_INVALID_ARGUMENT, "select_topk: K out of range"};
+    launch_pack_selected(L->bt, L->ldb, L->a, L->lda, L->r, L->n, L->m, sel_dev, (int)k, (int)P, bt_out, a_out,
+                         as_stream(s));
+    PG_API_END
+}
+
+extern "C" int pg_prefill_packed(pg_layer L, const void* bt_packed, const void* a_packed, size_t k,
+                                 const int64_t* offs, size_t P, const void* x, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(L && bt_packed && a_packed && offs && x && y && P > 0, PG_INVALID_ARGUMENT,
+            "prefill_packed: bad arguments");
+    require(L->dt == PG_BF16 && L->n % 8 == 0, PG_INVALID_ARGUMENT, "prefill_packed: bf16 layers, n % 8 == 0");
+    if (k == 0 || k > (size_t)L->r) throw Error{PG_INVALID_ARGUMENT, "select_topk: K out of range"};
+    check_ydt(L->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const int kp = (int)round_up(k, 8);
+    const size_t ys = dtype_size(ydt);
+    size_t zbytes = 0;
+    for (size_t p = 0; p < P; ++p) zbytes += round_up((size_t)(offs[p + 1] - offs[p]) * kp * 2, 256);
+    Scratch z(zbytes, st);
+    std::vector<UmmaSpec> s1, s2;
+    size_t zo = 0;
+    for (size_t p = 0; p < P; ++p) {
+        const int64_t t0 = offs[p], T = offs[p + 1] - offs[p];
+        if (T <= 0) continue;
+        const void* bt = static_cast<const char*>(bt_packed) + p * (size_t)kp * L->ldb * 2;
+        const void* a = static_cast<const char*>(a_packed) + p * (size_t)L->m * kp * 2;
+        const void* xq = static_cast<const char*>(x) + t0 * L->n * 2;
+        void* yq = static_cast<char*>(y) + t0 * L->m * ys;
+        if (!prefill_ok(L->n, (int)T)) {  // a few tokens: the gather GEMV path over the packed arena
+            SlotMap sm;
+            sm.run0_len = kp;
+            sm.cap = kp;
+            run_forward(PG_BF16, bt, L->ldb, a, kp, sm, kp, L->n, L->m, xq, 0, (int)T, yq, ydt, st);
+            continue;
+        }
+        void* zq = z.as<char>() + zo;
+        zo += round_up((size_t)T * kp * 2, 256);
+        s1.push_back(UmmaSpec{xq, L->n, bt, L->ldb, zq, kp, (int)T, kp, L->n, 1});
+        s2.push_back(UmmaSpec{zq, kp, a, kp, yq, L->m, (int)T, L->m, kp, ydt == PG_BF16 ? 1 : 0});
+    }
+    if (!s1.empty()) {
+        launch_umma(s1, st);
+        launch_umma(s2, st);
+    }
     PG_API_END
 }
 

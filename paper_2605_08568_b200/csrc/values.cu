@@ -101,6 +101,82 @@ __global__ void k_gather_cols(const W* __restrict__ src, int64_t lds, const int3
     }
 }
 
+// K3 for routed batches (config-3 prefill): every prompt p of a batch packs its
+// own K selected experts sel[p*k + j] (device, ascending -- the router's
+// output, no host round trip) into contiguous zero-padded arenas
+//   bt_out[p][j][:]  = B^T[sel_pj][:]          (rows; 16-byte vectors)
+//   a_out [p][i][j]  = A[i][sel_pj]            (columns; A rows staged in smem)
+// for j < kp (kp = k rounded up to 8; padding rows / columns are zero).
+// Bytes: read B^T rows and A once per prompt-tile, write P * kp * (n + m) * 2.
+__global__ void k_pack_rows_batched(const int4* __restrict__ src, int64_t lds16, const int32_t* __restrict__ sel,
+                                    int k, int kp, int nv, int4* __restrict__ dst, int64_t ldd16) {
+    const int j = blockIdx.x, p = blockIdx.y;
+    int4* d = dst + ((int64_t)p * kp + j) * ldd16;
+    if (j >= k) {
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) d[v] = make_int4(0, 0, 0, 0);
+        return;
+    }
+    const int4* s = src + (int64_t)__ldg(sel + (int64_t)p * k + j) * lds16;
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) d[v] = ld_stream(s + v);
+}
+
+constexpr int kPackRows = 8;  // A rows staged per CTA (amortises each prompt's selection list)
+// (measured: staging every prompt's ids at once instead of one prompt at a
+// time was slower -- the random 2-byte shared-memory gathers bound the kernel)
+__global__ void __launch_bounds__(256) k_pack_cols_batched(const uint16_t* __restrict__ src, int64_t lds, int r,
+                                                           const int32_t* __restrict__ sel, int k, int kp, int P,
+                                                           int m, uint16_t* __restrict__ dst) {
+    extern __shared__ __align__(16) uint16_t arow[];  // [kPackRows][rs] A rows, then [kp] selection ids
+    const int rs = (r + 7) / 8 * 8;
+    int32_t* ssel = reinterpret_cast<int32_t*>(arow + kPackRows * rs);
+    const int i0 = blockIdx.x * kPackRows;
+    const int nrow = min(kPackRows, m - i0);
+    for (int e = threadIdx.x; e < nrow * (rs / 8); e += blockDim.x) {
+        const int rr = e / (rs / 8), c8 = e % (rs / 8);
+        const uint16_t* srow = src + (int64_t)(i0 + rr) * lds;
+        if ((lds % 8) == 0 && c8 * 8 + 8 <= r) {
+            *reinterpret_cast<int4*>(arow + rr * rs + c8 * 8) = ld_stream(srow + c8 * 8);
+        } else {
+            for (int q = 0; q < 8; ++q) arow[rr * rs + c8 * 8 + q] = c8 * 8 + q < r ? srow[c8 * 8 + q] : 0;
+        }
+    }
+    const int kv = kp / 8;
+    for (int p = 0; p < P; ++p) {
+        __syncthreads();  // rows staged / previous prompt's ids consumed
+        for (int j = threadIdx.x; j < kp; j += blockDim.x) ssel[j] = j < k ? __ldg(sel + (int64_t)p * k + j) : -1;
+        __syncthreads();
+        uint16_t* dp = dst + ((int64_t)p * m + i0) * kp;  // this CTA's rows of prompt p: contiguous
+        for (int e = threadIdx.x; e < nrow * kv; e += blockDim.x) {
+            const int rr = e / kv, j8 = (e % kv) * 8;
+            const uint16_t* ar = arow + rr * rs;
+            const int4 sa = *reinterpret_cast<const int4*>(ssel + j8), sb = *reinterpret_cast<const int4*>(ssel + j8 + 4);
+            const int id[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+            uint32_t v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = id[q] >= 0 ? ar[id[q]] : 0u;
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = v[2 * q] | (v[2 * q + 1] << 16);
+            *reinterpret_cast<uint4*>(dp + (int64_t)rr * kp + j8) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+void launch_pack_selected(const void* bt, int64_t ldb, const void* a, int64_t lda, int r, int n, int m,
+                          const int32_t* sel, int k, int P, void* bt_out, void* a_out, cudaStream_t st) {
+    const int kp = (k + 7) / 8 * 8;
+    if (P <= 0 || k <= 0) return;
+    k_pack_rows_batched<<<dim3(kp, P), 128, 0, st>>>(static_cast<const int4*>(bt), ldb / 8, sel, k, kp,
+                                                     (n + 7) / 8, static_cast<int4*>(bt_out), ldb / 8);
+    PG_LAUNCH_CHECK();
+    const size_t smem = (size_t)kPackRows * ((r + 7) / 8 * 8) * 2 + (size_t)kp * 4;
+    if (smem > 48 * 1024)
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_pack_cols_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pack_cols_batched<<<(m + kPackRows - 1) / kPackRows, 256, smem, st>>>(
+        static_cast<const uint16_t*>(a), lda, r, sel, k, kp, P, m, static_cast<uint16_t*>(a_out));
+    PG_LAUNCH_CHECK();
+}
+
 // ---------------------------------------------------------------------------
 // K4 stage 1: z[s, c] = sum_j Bt[row(s), j] * x[c, j]   (one warp per slot)
 // ---------------------------------------------------------------------------
