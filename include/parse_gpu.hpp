@@ -12,11 +12,18 @@
 //   router.hpp:49  select_topk(logits, K)         gpu::select_topk        bit-exact
 //   model.hpp:102  select_topk(score(mean_pool))  gpu::route              bit-exact (fused)
 //   pattern_cache.hpp:38  cosine                  gpu::cosine             bit-exact
-//   pattern_cache.hpp:104 retrieve                gpu::DeviceCache::retrieve / gpu::retrieve
-//   pattern_cache.hpp:120 cache_insert            gpu::DeviceCache::insert
+//   pattern_cache.hpp:104 retrieve(const PatternCache&, emb)  gpu::retrieve / gpu::DeviceCache::retrieve
+//   pattern_cache.hpp:120 cache_insert(PatternCache&, entry)  gpu::cache_insert / gpu::DeviceCache::insert
+//   pattern_cache.hpp:50  embed_prompt(core, prov, tokens)    gpu::embed_prompt (pooling on device, bit-exact)
 //   rank_experts.hpp:52   masked_forward          gpu::masked_forward     f64: <= 1e-10 rel
-//   exec_engine.hpp:113/194 aggregate_layout / aggregated_forward  gpu::DeviceAggregatedLayer
-//   toy_lm.hpp:68  ProjectionProvider             gpu::GpuProvider (RoutingProvider semantics)
+//   exec_engine.hpp:112   aggregate_layout<T>     gpu::aggregate_layout<T>  (same shared/residual split)
+//   exec_engine.hpp:193   aggregated_forward<T>   gpu::aggregated_forward<T>
+//   exec_engine.hpp:239   scattered_forward<T>    gpu::scattered_forward<T>
+//   exec_engine.hpp:275   ExecEngine<T>::build/forward/storage_overhead  gpu::ExecEngine<T>
+//   exec_engine.hpp:322   ExecProvider            gpu::ExecProvider
+//   toy_lm.hpp:68  ProjectionProvider             gpu::GpuProvider (RoutingProvider semantics;
+//                                                 f64 / f32 / bf16 resident storage)
+//   (also: gpu::DeviceAggregatedLayer, the round-1 f64 layout wrapper)
 //
 // Host-memory convenience: each call copies its operands to the device and the
 // result back (synchronous).  Serving code keeps handles resident and uses the
@@ -25,6 +32,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -132,50 +140,81 @@ inline double cosine(const std::vector<double>& a, const std::vector<double>& b)
 
 // Device mirror of a PatternCache's embeddings; patterns stay host-side and
 // RetrieveResult::pattern points into the source cache (pattern_cache.hpp:96).
+// Built from a const cache it serves retrieve only; from a mutable one it also
+// runs the miss-path insertion on both copies.
 class DeviceCache {
 public:
-    explicit DeviceCache(PatternCache& cache) : cache_(cache) {
-        check(pg_cache_create(&h_, cache.d_model, cache.capacity, cache.min_similarity));
-        std::vector<double> emb;
-        for (const auto& e : cache.entries) emb.insert(emb.end(), e.embedding.vec.begin(), e.embedding.vec.end());
-        check(pg_cache_load(h_, emb.data(), cache.entries.size()));
-    }
+    explicit DeviceCache(const PatternCache& cache) : cc_(&cache) { load(); }
+    explicit DeviceCache(PatternCache& cache) : cc_(&cache), mc_(&cache) { load(); }
     ~DeviceCache() { pg_cache_destroy(h_); }
     DeviceCache(const DeviceCache&) = delete;
     DeviceCache& operator=(const DeviceCache&) = delete;
 
     RetrieveResult retrieve(const PromptEmbedding& emb) const {
-        if (cache_.entries.empty()) throw std::runtime_error("empty cache");
+        if (cc_->entries.empty()) throw std::runtime_error("empty cache");
         DevBuf<double> q(emb.vec.data(), emb.vec.size());
         pg_retrieve_result r{};
-        check(pg_retrieve(h_, q.p, 0, &r, nullptr, nullptr, nullptr));
+        check(pg_retrieve(h_, q.p, /*exact_similarity=*/1, &r, nullptr, nullptr, nullptr));
         RetrieveResult out;
         out.entry = r.entry;
         out.similarity = r.similarity;
         out.hit = r.hit != 0;
-        out.pattern = &cache_.entries[r.entry].pattern;
+        out.pattern = &cc_->entries[r.entry].pattern;
         return out;
     }
     // cache_insert (pattern_cache.hpp:120-124): refused once at capacity
     bool insert(CacheEntry entry) {
+        if (!mc_) throw std::logic_error("DeviceCache: built from a const PatternCache");
         int ins = 0;
         check(pg_cache_insert(h_, entry.embedding.vec.data(), 0, &ins, nullptr));
-        if (ins) cache_.entries.push_back(std::move(entry));
+        if (ins) mc_->entries.push_back(std::move(entry));
         return ins != 0;
     }
+    const PatternCache& cache() const { return *cc_; }
 
 private:
-    PatternCache& cache_;
+    void load() {
+        check(pg_cache_create(&h_, cc_->d_model, cc_->capacity, cc_->min_similarity));
+        std::vector<double> emb;
+        for (const auto& e : cc_->entries) emb.insert(emb.end(), e.embedding.vec.begin(), e.embedding.vec.end());
+        check(pg_cache_load(h_, emb.data(), cc_->entries.size()));
+    }
+    const PatternCache* cc_ = nullptr;
+    PatternCache* mc_ = nullptr;
     pg_cache h_ = nullptr;
 };
 
-inline RetrieveResult retrieve(PatternCache& cache, const PromptEmbedding& emb) {
+// retrieve (pattern_cache.hpp:104-117), reference signature
+inline RetrieveResult retrieve(const PatternCache& cache, const PromptEmbedding& emb) {
     if (cache.entries.empty()) throw std::runtime_error("empty cache");
     DeviceCache dc(cache);
     return dc.retrieve(emb);
 }
 
+// cache_insert (pattern_cache.hpp:120-124), reference signature: the capacity
+// rule on the host list (the device copy, if any, is updated through
+// DeviceCache::insert)
+inline bool cache_insert(PatternCache& cache, CacheEntry entry) {
+    if (cache.entries.size() >= cache.capacity) return false;
+    cache.entries.push_back(std::move(entry));
+    return true;
+}
+inline bool cache_insert(DeviceCache& cache, CacheEntry entry) { return cache.insert(std::move(entry)); }
+
 // ---------------------------------------------------------------- layers
+template <typename T> struct DType;
+template <> struct DType<double> { static constexpr pg_dtype v = PG_F64; };
+template <> struct DType<float> { static constexpr pg_dtype v = PG_F32; };
+
+inline uint16_t f32_to_bf16(float f) {  // round to nearest even (NaN kept quiet)
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+// A FactorizedLayer resident on the device in f64, f32 or bf16 storage.
 class DeviceLayer {
 public:
     DeviceLayer(const FactorizedLayer& l, pg_dtype storage = PG_F64) : m_(l.m), n_(l.n), dt_(storage) {
@@ -187,15 +226,50 @@ public:
     pg_layer handle() const { return h_; }
     size_t m() const { return m_; }
     size_t n() const { return n_; }
+    pg_dtype dtype() const { return dt_; }
 
-    // masked_forward with f64 storage (rank_experts.hpp:52-72)
+    // masked_forward (rank_experts.hpp:52-72) in the storage dtype's arithmetic
+    // (f64 -> f64; f32 -> f32; bf16 storage -> f32 accumulation), y as double
     Matd forward(const RankSelection& sel, const Matd& x) const {
         if (x.rows() != n_) throw std::invalid_argument("masked_forward: bad X shape");
-        DevBuf<double> xd(x.data(), x.rows() * x.cols()), y(m_ * x.cols());
-        check(pg_masked_forward(h_, sel.indices.data(), sel.indices.size(), 0, xd.p, PG_FEATURE_MAJOR,
-                                x.cols(), y.p, PG_F64, nullptr));
-        Matd out(m_, x.cols());
-        std::vector<double> hy = y.host();
+        const size_t T = x.cols(), nx = x.rows() * T;
+        Matd out(m_, T);
+        if (dt_ == PG_F64) {
+            DevBuf<double> xd(x.data(), nx), y(m_ * T);
+            check(pg_masked_forward(h_, sel.indices.data(), sel.indices.size(), 0, xd.p, PG_FEATURE_MAJOR, T, y.p,
+                                    PG_F64, nullptr));
+            const std::vector<double> hy = y.host();
+            std::copy(hy.begin(), hy.end(), out.data());
+            return out;
+        }
+        std::vector<float> xf(nx);
+        for (size_t i = 0; i < nx; ++i) xf[i] = float(x.data()[i]);
+        DevBuf<float> y(m_ * T);
+        if (dt_ == PG_F32) {
+            DevBuf<float> xd(xf.data(), nx);
+            check(pg_masked_forward(h_, sel.indices.data(), sel.indices.size(), 0, xd.p, PG_FEATURE_MAJOR, T, y.p,
+                                    PG_F32, nullptr));
+        } else {
+            std::vector<uint16_t> xb(nx);
+            for (size_t i = 0; i < nx; ++i) xb[i] = f32_to_bf16(xf[i]);
+            DevBuf<uint16_t> xd(xb.data(), nx);
+            check(pg_masked_forward(h_, sel.indices.data(), sel.indices.size(), 0, xd.p, PG_FEATURE_MAJOR, T, y.p,
+                                    PG_F32, nullptr));
+        }
+        const std::vector<float> hy = y.host();
+        for (size_t i = 0; i < hy.size(); ++i) out.data()[i] = hy[i];
+        return out;
+    }
+
+    template <typename T>
+    Mat<T> forward_t(const RankSelection& sel, const Mat<T>& x) const {
+        if (DType<T>::v != dt_) throw std::invalid_argument("DeviceLayer: storage dtype differs from T");
+        if (x.rows() != n_) throw std::invalid_argument("masked_forward: bad X shape");
+        DevBuf<T> xd(x.data(), x.rows() * x.cols()), y(m_ * x.cols());
+        check(pg_masked_forward(h_, sel.indices.data(), sel.indices.size(), 0, xd.p, PG_FEATURE_MAJOR, x.cols(), y.p,
+                                DType<T>::v, nullptr));
+        Mat<T> out(m_, x.cols());
+        const std::vector<T> hy = y.host();
         std::copy(hy.begin(), hy.end(), out.data());
         return out;
     }
@@ -212,6 +286,7 @@ inline Matd masked_forward(const FactorizedLayer& layer, const RankSelection& se
 }
 
 // aggregate_layout + aggregated_forward (exec_engine.hpp:112-236), f64 storage
+// (round-1 wrapper, kept for existing callers; see AggregatedLayer<T> below)
 class DeviceAggregatedLayer {
 public:
     DeviceAggregatedLayer(const FactorizedLayer& layer, const std::vector<RankSelection>& patterns, double psi)
@@ -259,15 +334,213 @@ private:
     size_t m_, n_;
 };
 
+// ---- AggregatedLayer<T> (exec_engine.hpp:97-110) on the device: the same
+// reference-numbered structure (shared ids, per-pattern residual ids,
+// use_shared, arena_offset) as host metadata; the arena itself lives in HBM.
+template <typename T>
+struct AggregatedLayer {
+    std::size_t m = 0, n = 0, r_store = 0;
+    std::vector<std::uint32_t> shared_ids;
+    struct Residual {
+        std::vector<std::uint32_t> ids;
+        std::vector<std::uint8_t> use_shared;
+        std::size_t arena_offset = 0;
+    };
+    std::vector<Residual> residuals;
+    double psi = 0.9;
+    std::shared_ptr<DeviceLayer> layer;  // full factors, storage dtype of T
+    std::shared_ptr<pg_agg_s> arena;     // packed [shared | residual_0 | ...] arena
+};
+
+template <typename T>
+AggregatedLayer<T> aggregate_layout(const FactorizedLayer& layer, const std::vector<RankSelection>& patterns,
+                                    double psi, std::shared_ptr<DeviceLayer> dev = nullptr) {
+    AggregatedLayer<T> g;
+    g.m = layer.m;
+    g.n = layer.n;
+    g.r_store = layer.r_store;
+    g.psi = psi;
+    g.layer = dev ? dev : std::make_shared<DeviceLayer>(layer, DType<T>::v);
+    std::vector<uint32_t> flat;
+    std::vector<size_t> ks;
+    for (const auto& p : patterns) {
+        flat.insert(flat.end(), p.indices.begin(), p.indices.end());
+        ks.push_back(p.indices.size());
+    }
+    pg_agg h = nullptr;
+    check(pg_aggregate_layout(&h, g.layer->handle(), flat.data(), ks.data(), patterns.size(), psi, nullptr));
+    g.arena = std::shared_ptr<pg_agg_s>(h, [](pg_agg a) { pg_agg_destroy(a); });
+    size_t c = 0;
+    check(pg_agg_shared(h, &c, nullptr));
+    g.shared_ids.resize(c);
+    check(pg_agg_shared(h, &c, g.shared_ids.data()));
+    g.residuals.resize(patterns.size());
+    for (size_t p = 0; p < patterns.size(); ++p) {
+        auto& R = g.residuals[p];
+        size_t rc = 0, off = 0;
+        check(pg_agg_residual(h, p, &rc, nullptr, nullptr, nullptr));
+        R.ids.resize(rc);
+        R.use_shared.resize(g.shared_ids.size());
+        check(pg_agg_residual(h, p, &rc, R.ids.data(), &off, R.use_shared.data()));
+        R.arena_offset = off;
+    }
+    return g;
+}
+
+template <typename T>
+Mat<T> aggregated_forward(const AggregatedLayer<T>& g, std::size_t pattern_id, const Mat<T>& x,
+                          AccessTrace* trace = nullptr) {
+    if (pattern_id >= g.residuals.size()) throw std::out_of_range("unknown pattern");
+    if (x.rows() != g.n) throw std::invalid_argument("aggregated_forward: bad X shape");
+    if (trace) {
+        size_t c = 0;
+        check(pg_agg_trace(g.arena.get(), pattern_id, &c, nullptr));
+        std::vector<size_t> cols(c);
+        check(pg_agg_trace(g.arena.get(), pattern_id, &c, cols.data()));
+        trace->a_cols.insert(trace->a_cols.end(), cols.begin(), cols.end());
+        trace->b_cols.insert(trace->b_cols.end(), cols.begin(), cols.end());
+    }
+    DevBuf<T> xd(x.data(), x.rows() * x.cols()), y(g.m * x.cols());
+    check(pg_aggregated_forward(g.arena.get(), pattern_id, nullptr, xd.p, PG_FEATURE_MAJOR, x.cols(), y.p,
+                                DType<T>::v, nullptr));
+    Mat<T> out(g.m, x.cols());
+    const std::vector<T> hy = y.host();
+    std::copy(hy.begin(), hy.end(), out.data());
+    return out;
+}
+
+// scattered_forward (exec_engine.hpp:239-252): the selected columns of the full
+// factors in S order (host matrices in, result out; uploads the factors)
+template <typename T>
+Mat<T> scattered_forward(const Mat<T>& a_full, const Mat<T>& b_full, const RankSelection& sel, const Mat<T>& x,
+                         AccessTrace* trace = nullptr) {
+    if (a_full.cols() != b_full.cols()) throw std::invalid_argument("scattered_forward: factor mismatch");
+    FactorizedLayer fl;
+    fl.m = a_full.rows();
+    fl.n = b_full.rows();
+    fl.r_store = a_full.cols();
+    fl.K = sel.indices.size();
+    fl.A = a_full.template cast<double>();
+    fl.B = b_full.template cast<double>();
+    DeviceLayer dl(fl, DType<T>::v);
+    if (trace)
+        for (std::uint32_t e : sel.indices) {
+            trace->a_cols.push_back(e);
+            trace->b_cols.push_back(e);
+        }
+    return dl.forward_t<T>(sel, x);
+}
+
+// ExecEngine<T> (exec_engine.hpp:275-319): per tensor the full factors and the
+// aggregated layout, resident on the device; forward dispatches on the
+// aggregated / scattered variants exactly like the reference.
+template <typename T>
+struct ExecEngine {
+    struct Tensor {
+        std::shared_ptr<DeviceLayer> full;
+        AggregatedLayer<T> agg;
+    };
+    std::map<std::string, Tensor> tensors;
+    std::vector<SelectionMap> patterns;
+    double psi = 0.9;
+
+    static ExecEngine build(const FactorizedModel& fm, std::vector<SelectionMap> pats, double psi_val) {
+        ExecEngine eng;
+        eng.psi = psi_val;
+        eng.patterns = std::move(pats);
+        for (const auto& [id, layer] : fm.layers) {
+            Tensor t;
+            t.full = std::make_shared<DeviceLayer>(layer, DType<T>::v);
+            std::vector<RankSelection> sels;
+            for (const auto& p : eng.patterns) sels.push_back(p.at(id));
+            t.agg = aggregate_layout<T>(layer, sels, psi_val, t.full);
+            eng.tensors[id] = std::move(t);
+        }
+        return eng;
+    }
+
+    Mat<T> forward(const std::string& id, std::size_t pattern_id, const Mat<T>& x, ExecVariant v,
+                   AccessTrace* trace = nullptr) const {
+        const Tensor& t = tensors.at(id);
+        if (variant_aggregated(v)) return aggregated_forward(t.agg, pattern_id, x, trace);
+        const RankSelection& sel = patterns.at(pattern_id).at(id);
+        if (trace)
+            for (std::uint32_t e : sel.indices) {
+                trace->a_cols.push_back(e);
+                trace->b_cols.push_back(e);
+            }
+        return t.full->template forward_t<T>(sel, x);
+    }
+
+    double storage_overhead() const {
+        double dup = 0, base = 0;
+        for (const auto& [id, t] : tensors) {
+            base += double(t.agg.r_store) * double(t.agg.m + t.agg.n);
+            for (const auto& r : t.agg.residuals) dup += double(r.ids.size()) * double(t.agg.m + t.agg.n);
+        }
+        return dup / base;
+    }
+};
+
+// ExecProvider (exec_engine.hpp:322-348): plan-driven full-LM serving (f64)
+class ExecProvider : public ProjectionProvider {
+public:
+    ExecProvider(const ExecEngine<double>& eng, std::size_t pattern_id, ExecVariant v)
+        : eng_(eng), pattern_(pattern_id), variant_(v) {}
+    Matd apply(std::size_t b, const char* p, const Matd& x) const {
+        ++launches_;
+        return eng_.forward(tensor_id(b, p), pattern_, x, variant_);
+    }
+    void qkv(std::size_t b, const Matd& hn, Matd& q, Matd& k, Matd& v) const override {
+        q = apply(b, "q", hn);
+        k = apply(b, "k", hn);
+        v = apply(b, "v", hn);
+    }
+    Matd o_proj(std::size_t b, const Matd& x) const override { return apply(b, "o", x); }
+    void upgate(std::size_t b, const Matd& hn, Matd& up, Matd& gate) const override {
+        up = apply(b, "up", hn);
+        gate = apply(b, "gate", hn);
+    }
+    Matd down_proj(std::size_t b, const Matd& x) const override { return apply(b, "down", x); }
+    std::size_t launches() const { return launches_; }
+
+private:
+    const ExecEngine<double>& eng_;
+    std::size_t pattern_;
+    ExecVariant variant_;
+    mutable std::size_t launches_ = 0;
+};
+
+// embed_prompt (pattern_cache.hpp:50-65): the block-0 forward through `prov`
+// (the reference's forward_lm with any ProjectionProvider -- e.g. a GpuProvider
+// or the static-prefix FactorizedProvider), then mean-pool + L2-normalise on
+// the device (pg_embed_normalize: bit-exact pooling).
+inline PromptEmbedding embed_prompt(const LmCore& core, const ProjectionProvider& prov,
+                                    const std::vector<std::uint8_t>& tokens, const std::string& source = "") {
+    if (tokens.empty()) throw std::invalid_argument("embed_prompt: empty prompt");
+    std::vector<Matd> blocks;
+    Capture cap;
+    cap.block_outputs = true;
+    cap.blocks = &blocks;
+    KVCacheState kvc(core.cfg.n_blocks);
+    forward_lm(core, prov, tokens, kvc, &cap);
+    const Matd& b0 = blocks.front();
+    DevBuf<double> xd(b0.data(), b0.rows() * b0.cols()), e(b0.rows());
+    check(pg_embed_normalize(xd.p, PG_F64, PG_FEATURE_MAJOR, b0.rows(), b0.cols(), e.p, nullptr));
+    return {e.host(), source};
+}
+
 // ---------------------------------------------------------------- provider
 // RoutingProvider semantics (model.hpp:90-126) on the GPU: route once per
 // tensor id from the first call's input, reuse the frozen selection after.
+// `storage`: f64 (reference arithmetic), f32 or bf16 (f32 accumulation) device
+// copies of every layer, resident for the provider's lifetime.
 class GpuProvider : public ProjectionProvider {
 public:
-    explicit GpuProvider(const FactorizedModel& m) : m_(m) {
+    explicit GpuProvider(const FactorizedModel& m, pg_dtype storage = PG_F64) : m_(m) {
         if (m.routers.empty()) throw std::runtime_error("model has no trained routers");
         for (const auto& [id, l] : m.layers) {
-            layers_.emplace(id, std::make_unique<DeviceLayer>(l, PG_F64));
+            layers_.emplace(id, std::make_unique<DeviceLayer>(l, storage));
             routers_.emplace(id, std::make_unique<DeviceRouter>(m.routers.at(id)));
         }
     }

@@ -8,10 +8,17 @@
 //  2. drop-in: forward_lm (toy_lm.hpp:201) with parse::gpu::GpuProvider vs the
 //     reference RoutingProvider (model.hpp:90-126) on a compressed toy model
 //     with random routers: identical selections, logits within 1e-9, and the
-//     frozen selection reused by decode_step (toy_lm.hpp:274).
+//     frozen selection reused by decode_step (toy_lm.hpp:274);
+//  3. the reference's exec-engine test cases (test_exec_engine.cpp:128-226)
+//     against parse::gpu::{aggregate_layout<T>, aggregated_forward<T>,
+//     scattered_forward<T>, ExecEngine<T>, ExecProvider};
+//  4. embed_prompt, retrieve(const PatternCache&), cache_insert, and the f32 /
+//     bf16 resident GpuProvider through forward_lm.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <numeric>
 
 #include "parse/corpus.hpp"
 #include "parse_gpu.hpp"
@@ -43,6 +50,43 @@ static double max_rel(const Matd& a, const Matd& b) {
         s = std::max(s, std::abs(b.raw()[i]));
     }
     return d / s;
+}
+
+// the reference test's toy model (test_exec_engine.cpp:12-27 configuration)
+static FactorizedModel small_model() {
+    ToyLMConfig cfg;
+    cfg.n_blocks = 2;
+    cfg.d_model = 16;
+    cfg.n_heads = 2;
+    cfg.n_kv_heads = 2;
+    cfg.d_ff = 24;
+    cfg.max_seq = 128;
+    cfg.seed = 91;
+    const DenseModel dense = init_dense_model(cfg);
+    const auto calib = sample_calibration({DomainKind::markov_text, 1, 0}, 8, 24, 3);
+    CompressionConfig cc;
+    cc.ratio = 0.3;
+    return compress_model(dense, calib, cc);
+}
+
+// prefix-biased random K-subsets per tensor (the reference test's generator rule)
+static std::vector<SelectionMap> patterns_for(const FactorizedModel& fm, std::size_t count, std::uint64_t seed) {
+    Rng rng(seed);
+    std::vector<SelectionMap> pats(count);
+    for (auto& p : pats)
+        for (const auto& [id, layer] : fm.layers) {
+            std::vector<std::uint32_t> pool(layer.r_store);
+            std::iota(pool.begin(), pool.end(), 0u);
+            RankSelection sel;
+            for (std::size_t i = 0; i < layer.K; ++i) {
+                const std::size_t pick = rng.below(2) ? 0 : rng.below(pool.size());
+                sel.indices.push_back(pool[pick]);
+                pool.erase(pool.begin() + std::ptrdiff_t(pick));
+            }
+            std::sort(sel.indices.begin(), sel.indices.end());
+            p[id] = std::move(sel);
+        }
+    return pats;
 }
 
 int main() {
@@ -161,6 +205,169 @@ int main() {
         bool still = true;
         for (const auto& [id, s] : ref.selections()) still = still && dev.selections().at(id).indices == s.indices;
         EXPECT(still, "decode never re-routes");
+    }
+    // ---- 3. exec engine on the device (test_exec_engine.cpp:128-226)
+    {
+        const FactorizedModel fm = small_model();
+        const auto pats = patterns_for(fm, 4, 17);
+        const auto eng = gpu::ExecEngine<double>::build(fm, pats, 0.5);
+        const auto ref_eng = ExecEngine<double>::build(fm, pats, 0.5);
+        bool same_layout = true;
+        for (const auto& [id, t] : ref_eng.tensors) {
+            const auto& g = eng.tensors.at(id).agg;
+            same_layout = same_layout && g.shared_ids == t.agg.shared_ids;
+            for (std::size_t p = 0; p < pats.size(); ++p)
+                same_layout = same_layout && g.residuals[p].ids == t.agg.residuals[p].ids &&
+                              g.residuals[p].use_shared == t.agg.residuals[p].use_shared &&
+                              g.residuals[p].arena_offset == t.agg.residuals[p].arena_offset;
+        }
+        EXPECT(same_layout, "ExecEngine<double>::build: shared / residual / use_shared / arena_offset as the reference");
+        Rng rng(19);
+        double worst = 0;
+        bool agg_pair = true, scat_pair = true;
+        for (const auto& [id, layer] : fm.layers) {
+            Matd x(layer.n, 6);
+            for (double& v : x.raw()) v = rng.gaussian();
+            for (std::size_t pid = 0; pid < pats.size(); ++pid) {
+                const Matd ref = masked_forward(layer, pats[pid].at(id), x);
+                const Matd a1 = eng.forward(id, pid, x, ExecVariant::aggregated_only);
+                const Matd a2 = eng.forward(id, pid, x, ExecVariant::aggregated_fused);
+                const Matd s1 = eng.forward(id, pid, x, ExecVariant::scattered_unfused);
+                const Matd s2 = eng.forward(id, pid, x, ExecVariant::fused_only);
+                for (const Matd* m : {&a1, &a2, &s1, &s2}) worst = std::max(worst, max_rel(*m, ref));
+                agg_pair = agg_pair && a1.raw() == a2.raw();
+                scat_pair = scat_pair && s1.raw() == s2.raw();
+                const Matd sf = gpu::scattered_forward(ref_eng.tensors.at(id).a_full, ref_eng.tensors.at(id).b_full,
+                                                       pats[pid].at(id), x);
+                scat_pair = scat_pair && sf.raw() == s1.raw();
+            }
+        }
+        std::printf("     four variants vs masked_forward: max rel %.3e\n", worst);
+        EXPECT(worst <= 1e-12, "all four variants vs masked_forward, f64 <= 1e-12 (test_exec_engine.cpp:128-146)");
+        EXPECT(agg_pair && scat_pair, "aggregated variants bit-identical to each other, scattered likewise");
+
+        const auto pats3 = patterns_for(fm, 3, 23);
+        const auto engf = gpu::ExecEngine<float>::build(fm, pats3, 0.5);
+        Rng rf(29);
+        bool close = true;
+        for (const auto& [id, layer] : fm.layers) {
+            Matd x(layer.n, 4);
+            for (double& v : x.raw()) v = rf.gaussian();
+            const Matf xf = x.cast<float>();
+            for (std::size_t pid = 0; pid < pats3.size(); ++pid) {
+                const Matd ref = masked_forward(layer, pats3[pid].at(id), x);
+                const Matf got = engf.forward(id, pid, xf, ExecVariant::aggregated_fused);
+                for (std::size_t i = 0; i < ref.raw().size(); ++i)
+                    close = close && std::abs(double(got.raw()[i]) - ref.raw()[i]) < 1e-5 * (1.0 + std::abs(ref.raw()[i]));
+            }
+        }
+        EXPECT(close, "float engine within 1e-5 (1 + |ref|) of the double reference (:148-165)");
+
+        bool runs = true;
+        Rng rt(37);
+        for (const auto& [id, layer] : fm.layers) {
+            Matd x(layer.n, 2);
+            for (double& v : x.raw()) v = rt.gaussian();
+            for (std::size_t pid = 0; pid < pats.size(); ++pid) {
+                AccessTrace tr, sc;
+                eng.forward(id, pid, x, ExecVariant::aggregated_fused, &tr);
+                const auto& agg = eng.tensors.at(id).agg;
+                runs = runs && tr.a_cols.size() == agg.shared_ids.size() + agg.residuals[pid].ids.size();
+                runs = runs && maximal_runs(tr.a_cols).size() <= 2 && maximal_runs(tr.b_cols).size() <= 2;
+                eng.forward(id, pid, x, ExecVariant::scattered_unfused, &sc);
+                const std::vector<std::size_t> want(pats[pid].at(id).indices.begin(), pats[pid].at(id).indices.end());
+                runs = runs && sc.a_cols == want;
+            }
+        }
+        EXPECT(runs, "aggregated trace <= 2 contiguous runs, scattered trace = S (:167-193)");
+
+        auto one = patterns_for(fm, 1, 41);
+        const std::vector<SelectionMap> same = {one[0], one[0], one[0]};
+        const auto varied = patterns_for(fm, 4, 43);
+        EXPECT(gpu::ExecEngine<double>::build(fm, same, 0.9).storage_overhead() == 0.0 &&
+                   gpu::ExecEngine<double>::build(fm, varied, 0.9).storage_overhead() ==
+                       ExecEngine<double>::build(fm, varied, 0.9).storage_overhead(),
+               "storage_overhead as the reference (:195-208)");
+
+        const auto p2 = patterns_for(fm, 2, 47);
+        const auto eng2 = gpu::ExecEngine<double>::build(fm, p2, 0.5);
+        const auto toks = sample_calibration({DomainKind::markov_text, 5, 0}, 1, 12, 9)[0];
+        double lm_worst = 0;
+        for (std::size_t pid = 0; pid < p2.size(); ++pid) {
+            const FactorizedProvider ref_prov(fm, &p2[pid]);
+            KVCacheState kv1(fm.core.cfg.n_blocks);
+            const Matd ref = forward_lm(fm.core, ref_prov, toks, kv1);
+            for (ExecVariant v : {ExecVariant::scattered_unfused, ExecVariant::aggregated_fused}) {
+                const gpu::ExecProvider prov(eng2, pid, v);
+                KVCacheState kv2(fm.core.cfg.n_blocks);
+                lm_worst = std::max(lm_worst, max_rel(forward_lm(fm.core, prov, toks, kv2), ref));
+            }
+        }
+        std::printf("     ExecProvider full LM vs FactorizedProvider: max rel %.3e\n", lm_worst);
+        EXPECT(lm_worst <= 1e-9, "ExecProvider serves the full LM like the masked provider, <= 1e-9 (:210-226)");
+
+        bool threw = false;
+        try {
+            gpu::aggregated_forward(eng.tensors.begin()->second.agg, 99, Matd(16, 1));
+        } catch (const std::out_of_range&) {
+            threw = true;
+        }
+        EXPECT(threw, "aggregated_forward unknown pattern -> out_of_range");
+    }
+    // ---- 4. embed_prompt, const retrieve, cache_insert, f32 / bf16 GpuProvider
+    {
+        FactorizedModel fm = small_model();
+        const FactorizedProvider static_prov(fm);  // the embedding model (pattern_cache.hpp:84)
+        PatternCache cache;
+        cache.d_model = fm.core.cfg.d_model;
+        cache.capacity = 3;
+        cache.min_similarity = 0.8;
+        const auto prompts = sample_calibration({DomainKind::markov_text, 5, 0}, 4, 16, 11);
+        bool emb_exact = true;
+        for (std::size_t i = 0; i < 3; ++i) {
+            const PromptEmbedding ref = embed_prompt(fm.core, static_prov, prompts[i]);
+            const PromptEmbedding got = gpu::embed_prompt(fm.core, static_prov, prompts[i]);
+            emb_exact = emb_exact && got.vec == ref.vec;
+            CacheEntry e;
+            e.embedding = got;
+            e.pattern = patterns_for(fm, 1, 60 + i)[0];
+            EXPECT(gpu::cache_insert(cache, e), "cache_insert below capacity");
+        }
+        EXPECT(emb_exact, "embed_prompt: device pooling bit-identical to the reference");
+        CacheEntry extra;
+        extra.embedding = gpu::embed_prompt(fm.core, static_prov, prompts[3]);
+        EXPECT(!gpu::cache_insert(cache, extra) && cache.entries.size() == 3, "cache_insert refused at capacity");
+        const PatternCache& cc = cache;
+        bool rr = true;
+        for (std::size_t i = 0; i < 4; ++i) {
+            const PromptEmbedding q = embed_prompt(fm.core, static_prov, prompts[i]);
+            const RetrieveResult a = gpu::retrieve(cc, q), b = retrieve(cc, q);
+            rr = rr && a.entry == b.entry && a.hit == b.hit && a.pattern == b.pattern && a.similarity == b.similarity;
+        }
+        EXPECT(rr, "retrieve(const PatternCache&): entry, hit, pattern pointer, similarity as the reference");
+
+        std::uint64_t seed = 300;
+        for (const auto& [id, layer] : fm.layers) {
+            RouterParams p = make_router(layer.r_store, layer.n);
+            p.theta = random_mat(layer.r_store, layer.n, ++seed);
+            fm.routers[id] = std::move(p);
+        }
+        const auto toks = sample_calibration({DomainKind::markov_text, 5, 0}, 1, 12, 9)[0];
+        RoutingProvider ref(fm);
+        KVCacheState kv0(fm.core.cfg.n_blocks);
+        const Matd l0 = forward_lm(fm.core, ref, toks, kv0);
+        for (pg_dtype dt : {PG_F32, PG_BF16}) {
+            gpu::GpuProvider dev(fm, dt);
+            KVCacheState kv(fm.core.cfg.n_blocks);
+            const Matd l = forward_lm(fm.core, dev, toks, kv);
+            bool sel_same = true;
+            for (const auto& [id, s] : ref.selections()) sel_same = sel_same && dev.selections().at(id).indices == s.indices;
+            const double e = max_rel(l, l0);
+            std::printf("     GpuProvider %s storage: logits max rel %.3e\n", dt == PG_F32 ? "f32" : "bf16", e);
+            EXPECT(sel_same && e <= (dt == PG_F32 ? 1e-4 : 5e-2),
+                   dt == PG_F32 ? "f32 GpuProvider: same routes, logits <= 1e-4"
+                                : "bf16 GpuProvider: same routes, logits <= 5e-2");
+        }
     }
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "PASSED", g_fail);
     return g_fail ? 1 : 0;
