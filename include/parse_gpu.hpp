@@ -23,6 +23,8 @@
 //   exec_engine.hpp:322   ExecProvider            gpu::ExecProvider
 //   toy_lm.hpp:68  ProjectionProvider             gpu::GpuProvider (RoutingProvider semantics;
 //                                                 f64 / f32 / bf16 resident storage)
+//   pattern_cache.hpp:67  route_prompt            gpu::route_prompt (GpuProvider prefill)
+//   retrieve-or-route serving composition         gpu::select_for_prompt (hit: cached S; miss: route + insert)
 //   (also: gpu::DeviceAggregatedLayer, the round-1 f64 layout wrapper)
 //
 // Host-memory convenience: each call copies its operands to the device and the
@@ -570,6 +572,48 @@ private:
     std::map<std::string, std::unique_ptr<DeviceRouter>> routers_;
     mutable SelectionMap selections_;
 };
+
+// ---------------------------------------------------------------- serving composition
+// route_prompt (pattern_cache.hpp:67-73) on the GPU: the prompt's prefill
+// through GpuProvider (bit-exact routing), its frozen selections returned
+inline SelectionMap route_prompt(const FactorizedModel& fm, const std::vector<std::uint8_t>& tokens) {
+    GpuProvider prov(fm);
+    KVCacheState kvc(fm.core.cfg.n_blocks);
+    forward_lm(fm.core, prov, tokens, kvc);
+    return prov.selections();
+}
+
+struct PromptSelection {
+    SelectionMap pattern;      // the subsets the prompt is served with (prefill + every decode step)
+    RetrieveResult retrieved;  // retrieve's answer (similarity -2 when the cache was empty)
+    bool routed = false;       // miss: routed online
+    bool inserted = false;     // miss: cache_insert accepted the routed pattern
+};
+
+// Retrieve-or-route (the north star's "S chosen by the router or by a
+// pattern-cache lookup"): embed with the static-prefix model
+// (pattern_cache.hpp:84), retrieve (:104-117); hit -> the entry's pattern;
+// miss -> route_prompt + cache_insert (:120-124, refused at capacity).
+inline PromptSelection select_for_prompt(const FactorizedModel& fm, DeviceCache& cache,
+                                         const std::vector<std::uint8_t>& tokens) {
+    const FactorizedProvider emb_prov(fm);
+    PromptEmbedding emb = gpu::embed_prompt(fm.core, emb_prov, tokens);
+    PromptSelection out;
+    if (!cache.cache().entries.empty()) {
+        out.retrieved = cache.retrieve(emb);
+        if (out.retrieved.hit) {
+            out.pattern = *out.retrieved.pattern;
+            return out;
+        }
+    }
+    out.routed = true;
+    out.pattern = gpu::route_prompt(fm, tokens);
+    CacheEntry e;
+    e.embedding = std::move(emb);
+    e.pattern = out.pattern;
+    out.inserted = cache.insert(std::move(e));
+    return out;
+}
 
 }  // namespace gpu
 }  // namespace parse

@@ -888,6 +888,74 @@ class ExecProvider(ProjectionProvider):
         return self.eng.forward(tensor_id(b, p), self.pattern, x, self.variant, layout=self.layout)
 
 
+# ---------------------------------------------------------------- serving composition
+@dataclass
+class PromptSelection:
+    """The frozen per-tensor expert subsets a prompt is served with, and where
+    they came from: "hit" (a cached entry's SelectionMap) or "routed" (online
+    routing on the prompt's prefill inputs)."""
+    pattern: dict
+    source: str
+    entry: int = -1           # cache entry serving / now holding the pattern (-1: not cached)
+    similarity: float = -2.0  # retrieve's best cosine (-2 for an empty cache)
+    inserted: bool = False    # miss path: cache_insert accepted the routed pattern
+
+
+class PatternServer:
+    """Retrieve-or-route serving (the north star's "S chosen by a linear router or
+    by a pattern-cache lookup, then reused across decode steps"):
+
+      retrieve(cache, embedding)                       pattern_cache.hpp:104-117
+        hit  (sim >= min_similarity): the entry's SelectionMap
+        miss: route every tensor id from the input it sees at prefill,
+              select_topk(score(mean_pool(x)), K)      model.hpp:96-106 (route_prompt, pattern_cache.hpp:67-73)
+              then cache_insert(cache, {embedding, S}) pattern_cache.hpp:120-124 (refused at capacity)
+
+    The packed device layouts (aggregate_layout, exec_engine.hpp:112-164) are
+    cached per cache entry, so repeated hits on an entry never re-pack; decode
+    steps reuse the prompt's frozen selection (provider())."""
+
+    def __init__(self, model: FactorizedModel, cache: PatternCache, psi: float = 0.9):
+        self.model, self.cache, self.psi = model, cache, psi
+        self._packs: dict[int, dict] = {}
+        self.packs_built = 0
+
+    def select_for_prompt(self, embedding, route_inputs, layout: str = "feature") -> PromptSelection:
+        """embedding: PromptEmbedding (or its vector); route_inputs: {tensor id:
+        x} or a callable tid -> x giving the input each routed linear sees at
+        prefill (n x T feature-major, or T x n with layout="token")."""
+        emb = embedding if isinstance(embedding, PromptEmbedding) else PromptEmbedding(np.asarray(embedding))
+        sim = -2.0
+        if self.cache.entries:
+            res = retrieve(self.cache, emb, exact_similarity=True)  # the reference's RetrieveResult, bit for bit
+            sim = res.similarity
+            if res.hit:
+                return PromptSelection(res.pattern, "hit", res.entry, res.similarity, False)
+        get = route_inputs if callable(route_inputs) else route_inputs.__getitem__
+        pattern = {}
+        for tid, layer in self.model.layers.items():
+            x = get(tid)
+            sel = route_select(self.model.routers[tid], x, layer.K, layout=layout)[0]
+            pattern[tid] = RankSelection(sel.cpu().numpy().astype(np.uint32))
+        inserted = cache_insert(self.cache, CacheEntry(emb, pattern))
+        return PromptSelection(pattern, "routed", len(self.cache.entries) - 1 if inserted else -1, sim, inserted)
+
+    def layouts(self, sel: PromptSelection) -> dict:
+        """Per tensor id, the prompt's packed layout (one pattern).  Cached per
+        cache entry: a second hit on the same entry reuses the packs."""
+        if sel.entry >= 0 and sel.entry in self._packs:
+            return self._packs[sel.entry]
+        packs = {tid: aggregate_layout(self.model.layers[tid], [s], self.psi) for tid, s in sel.pattern.items()}
+        self.packs_built += 1
+        if sel.entry >= 0:
+            self._packs[sel.entry] = packs
+        return packs
+
+    def provider(self, sel: PromptSelection, layout: str = "feature") -> "FactorizedProvider":
+        """Serve prefill and every decode step with the frozen selection."""
+        return FactorizedProvider(self.model, sel.pattern, layout=layout)
+
+
 def _pattern_args(pattern_ids, count):
     if isinstance(pattern_ids, torch.Tensor):
         return None, _ptr(pattern_ids)

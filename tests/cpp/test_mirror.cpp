@@ -369,6 +369,37 @@ int main() {
                                 : "bf16 GpuProvider: same routes, logits <= 5e-2");
         }
     }
+    // ---- 5. retrieve-or-route composition vs the reference build_cache / route_prompt
+    {
+        FactorizedModel fm = small_model();
+        std::uint64_t seed = 500;
+        for (const auto& [id, layer] : fm.layers) {
+            RouterParams p = make_router(layer.r_store, layer.n);
+            p.theta = random_mat(layer.r_store, layer.n, ++seed);
+            fm.routers[id] = std::move(p);
+        }
+        const auto prompts = sample_calibration({DomainKind::markov_text, 5, 0}, 5, 16, 21);
+        const std::vector<std::vector<std::uint8_t>> first(prompts.begin(), prompts.begin() + 3);
+        PatternCache cache = build_cache(fm, first, 0.99999, 4);  // reference: embeddings + routed patterns
+        gpu::DeviceCache dc(cache);
+        const auto s1 = gpu::select_for_prompt(fm, dc, prompts[1]);
+        bool same_pat = s1.pattern.size() == cache.entries[1].pattern.size();
+        for (const auto& [id, sel] : cache.entries[1].pattern)
+            same_pat = same_pat && s1.pattern.count(id) && s1.pattern.at(id).indices == sel.indices;
+        EXPECT(!s1.routed && s1.retrieved.hit && s1.retrieved.entry == 1 && same_pat,
+               "select_for_prompt: cached prompt hits its own entry and serves its pattern");
+        const RetrieveResult want = retrieve(cache, embed_prompt(fm.core, FactorizedProvider(fm), prompts[3]));
+        const auto s3 = gpu::select_for_prompt(fm, dc, prompts[3]);
+        bool same_route = s3.pattern.size() == fm.layers.size();
+        const SelectionMap ref_route = route_prompt(fm, prompts[3]);
+        for (const auto& [id, sel] : ref_route) same_route = same_route && s3.pattern.at(id).indices == sel.indices;
+        EXPECT(!want.hit && s3.routed && same_route && s3.inserted && cache.entries.size() == 4,
+               "select_for_prompt: a miss routes exactly like route_prompt and is inserted");
+        const auto s4 = gpu::select_for_prompt(fm, dc, prompts[4]);
+        EXPECT(s4.routed && !s4.inserted && cache.entries.size() == 4, "select_for_prompt: at capacity, not inserted");
+        const auto s3b = gpu::select_for_prompt(fm, dc, prompts[3]);
+        EXPECT(!s3b.routed && s3b.retrieved.entry == 3, "select_for_prompt: the routed prompt now hits its entry");
+    }
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "PASSED", g_fail);
     return g_fail ? 1 : 0;
 }
