@@ -239,6 +239,30 @@ int pg_module_forward_union(const pg_layer* layers, const uint8_t* const* masks_
                             size_t n_linears, const int32_t* tok_pat_dev, size_t T, const void* x_dev,
                             void* const* ys_dev, pg_dtype y_dtype, pg_stream stream);
 
+/* A whole heterogeneous decode step as ONE persistent launch (config 4):
+ * the union program records modules (linears sharing an input, as
+ * pg_module_forward_union, T <= 256 tokens) and runs all their GEMM stages in
+ * one launch, each k-block of a stage waiting (device-side ready counters) for
+ * the output tile of the stage that produces it, weights streamed across stage
+ * and layer boundaries.  The executed form of the reference's ExecPlan
+ * (exec_engine.hpp:19-68: fused_B / batched_A per module) for a whole stack.
+ * x_dev / ys_dev addresses are bound at add time; a module whose x_dev is an
+ * earlier module's output consumes it tile by tile.  Every output buffer must
+ * be distinct and never overwrite an input of an earlier module (per-layer
+ * buffers).  The first pg_union_prog_run allocates the workspace (not
+ * capturable); later runs are single launches, capturable in CUDA graphs. */
+typedef struct pg_union_prog_s* pg_union_prog;
+int pg_union_prog_create(pg_union_prog* out, size_t T);
+int pg_union_prog_add_module(pg_union_prog prog, const pg_layer* layers, const uint8_t* const* masks_dev,
+                             const size_t* P, size_t n_linears, const void* x_dev, void* const* ys_dev,
+                             pg_dtype y_dtype);
+int pg_union_prog_run(pg_union_prog prog, const int32_t* tok_pat_dev, pg_stream stream);
+int pg_union_prog_info(pg_union_prog prog, size_t* phases, size_t* grid);
+int pg_union_prog_destroy(pg_union_prog prog);
+/* Diagnostics: with PG_PROG_DBG=1 at the first run, per-CTA %globaltimer stamps
+ * [grid][64] of the last run (*have = 0 otherwise). */
+int pg_union_prog_debug(pg_union_prog prog, uint64_t* out_host, size_t n, int* have);
+
 /* Expert-sharded decode (BASELINE config 5) with the all-reduce fused into
  * the rank-expert kernel: rank `rank` of `npeer` serves its expert shard
  * (aggregated layout of its experts, `pattern` = the local selection) for one

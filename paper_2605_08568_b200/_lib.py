@@ -86,6 +86,12 @@ _SIGS = {
     "pg_selection_masks": [_vp, _vp, _vp, _sz, _vp, _vp],
     "pg_masked_forward_union": [_vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],
     "pg_module_forward_union": [_vp, _vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],
+    "pg_union_prog_create": [C.POINTER(_vp), _sz],
+    "pg_union_prog_add_module": [_vp, _vp, _vp, _vp, _sz, _vp, _vp, _i],
+    "pg_union_prog_run": [_vp, _vp, _vp],
+    "pg_union_prog_info": [_vp, C.POINTER(_sz), C.POINTER(_sz)],
+    "pg_union_prog_destroy": [_vp],
+    "pg_union_prog_debug": [_vp, _vp, _sz, C.POINTER(_i)],
     "pg_module_forward": [C.POINTER(_vp), _sz, _sp, _vp, _vp, C.POINTER(_vp), _i, _vp],
     "pg_prefill_batched": [C.POINTER(_vp), _i64p, _sz, _vp, _vp, _i, _vp],
     "pg_gemm_bf16": [_vp, C.c_int64, _vp, C.c_int64, _vp, C.c_int64, _sz, _sz, _sz, _i, _vp],

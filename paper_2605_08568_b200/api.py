@@ -498,6 +498,76 @@ def module_forward_union(layers, batches, token_patterns, x: torch.Tensor, out_d
     return ys
 
 
+class UnionProgram:
+    """A whole heterogeneous decode step as ONE persistent launch
+    (pg_union_prog_*, union_prog.cu): modules are recorded with
+    add_module (the arguments of module_forward_union, minus the token
+    patterns) and run() executes every stage of every module in one kernel,
+    each stage's k-blocks waiting on device for the output tiles they read.
+    Buffers are bound at add time; a module whose x is an earlier module's
+    output consumes it tile by tile.  Outputs must be distinct buffers that
+    no earlier module reads (e.g. per-layer activations).  The executed form
+    of build_plan (exec_engine.hpp:19-68) for a stack of layers."""
+
+    def __init__(self, T: int):
+        self.T = int(T)
+        h = C.c_void_p()
+        call("pg_union_prog_create", C.byref(h), self.T)
+        self.handle = h
+        self._keep = []  # tensors whose addresses the program holds
+        self._P = None
+
+    def add_module(self, layers, batches, x: torch.Tensor, outs) -> None:
+        if len(layers) != len(batches) or not layers or len(outs) != len(layers):
+            raise ValueError("union_program: one selection batch and one output per layer")
+        for L, b in zip(layers, batches):
+            if b.layer is not L:
+                raise ValueError("union_program: selection batch built for another layer")
+        if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous() or tuple(x.shape) != (self.T, layers[0].n):
+            raise ValueError("union_program: x must be a contiguous bf16 device tensor [T, n]")
+        ydt = _out_dtype(layers[0].dtype, outs[0].dtype)
+        for L, y in zip(layers, outs):
+            if tuple(y.shape) != (self.T, L.m) or not y.is_contiguous() or _out_dtype(L.dtype, y.dtype) != ydt:
+                raise ValueError("union_program: outputs must be contiguous [T, m] of one dtype")
+        n = len(layers)
+        hs = (C.c_void_p * n)(*[L.handle.value if hasattr(L.handle, "value") else L.handle for L in layers])
+        ms = (C.c_void_p * n)(*[_ptr(b.masks) for b in batches])
+        ps = (C.c_size_t * n)(*[b.P for b in batches])
+        yp = (C.c_void_p * n)(*[_ptr(y) for y in outs])
+        call("pg_union_prog_add_module", self.handle, hs, ms, ps, n, _ptr(x), yp, ydt)
+        self._keep += [x, *outs, *batches, *layers]
+        P = min(b.P for b in batches)
+        self._P = P if self._P is None else min(self._P, P)
+
+    def run(self, token_patterns) -> None:
+        if isinstance(token_patterns, torch.Tensor) and token_patterns.is_cuda:
+            tp = token_patterns
+            if tp.dtype != torch.int32 or not tp.is_contiguous():
+                raise ValueError("union_program: device token patterns must be contiguous int32")
+        else:
+            tpn = np.ascontiguousarray(token_patterns, dtype=np.int64)
+            if tpn.size and (tpn.min() < 0 or tpn.max() >= (self._P or 0)):
+                raise IndexError("union_program: unknown pattern")
+            tp = torch.from_numpy(tpn.astype(np.int32)).cuda()
+            self._tp = tp
+        if tp.numel() != self.T:
+            raise ValueError("union_program: one pattern id per token")
+        call("pg_union_prog_run", self.handle, _ptr(tp), _stream())
+
+    def info(self) -> tuple[int, int]:
+        ph, gr = C.c_size_t(), C.c_size_t()
+        call("pg_union_prog_info", self.handle, C.byref(ph), C.byref(gr))
+        return ph.value, gr.value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                call("pg_union_prog_destroy", h)
+            except Exception:
+                pass
+
+
 @dataclass
 class AccessTrace:
     """exec_engine.hpp:90-92."""

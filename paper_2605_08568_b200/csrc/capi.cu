@@ -11,6 +11,7 @@
 
 #include "chain.cuh"
 #include "umma.cuh"
+#include "union_prog.cuh"
 #include "union_wm.cuh"
 
 namespace pg {
@@ -1003,6 +1004,90 @@ int pg_module_forward_union(const pg_layer* Ls, const uint8_t* const* masks, con
     else if (!launch_umma_splitk_multi(s1, ws.p, st)) launch_umma(s1, st);
     if (wb) launch_union_wm(wm2, (int)T, nullptr, st);
     else if (!launch_umma_splitk_multi(s2, ws.p, st)) launch_umma(s2, st);
+    PG_API_END
+}
+
+// ------------------------------------------------------------ union program
+// A whole decode step of modules as one persistent launch (union_prog.cu).
+// Each module adds two phases: stage 1 into a program-owned Z buffer (the
+// selection mask in the epilogue), stage 2 from Z into the caller's outputs.
+struct pg_union_prog_s {
+    std::unique_ptr<pg::UnionProgram> prog;
+    size_t T;
+    std::vector<void*> z;  // per module: [T, r_pad] bf16 per linear, program-owned
+    ~pg_union_prog_s() {
+        for (void* p : z) cudaFree(p);
+    }
+};
+
+int pg_union_prog_create(pg_union_prog* out, size_t T) {
+    PG_API_BEGIN
+    require(out && T >= 1 && T <= 256, PG_INVALID_ARGUMENT, "union_prog_create: 1 <= T <= 256");
+    auto h = std::make_unique<pg_union_prog_s>();
+    h->prog = std::make_unique<UnionProgram>((int)T);
+    h->T = T;
+    *out = h.release();
+    PG_API_END
+}
+
+int pg_union_prog_add_module(pg_union_prog H, const pg_layer* Ls, const uint8_t* const* masks, const size_t* Ps,
+                             size_t nlin, const void* x, void* const* ys, pg_dtype ydt) {
+    PG_API_BEGIN
+    require(H && Ls && masks && Ps && x && ys && nlin >= 1 && nlin <= 4, PG_INVALID_ARGUMENT,
+            "union_prog_add_module: bad arguments (1..4 linears)");
+    const size_t T = H->T;
+    std::vector<size_t> zoff(nlin);
+    size_t zbytes = 0;
+    for (size_t l = 0; l < nlin; ++l) {
+        const pg_layer L = Ls[l];
+        require(L && masks[l] && ys[l] && Ps[l] > 0, PG_INVALID_ARGUMENT, "union_prog_add_module: bad arguments");
+        require(L->dt == PG_BF16 && L->n == Ls[0]->n && L->n % 8 == 0, PG_INVALID_ARGUMENT,
+                "union_prog_add_module: bf16 linears sharing one input width (multiple of 8)");
+        check_ydt(L->dt, ydt);
+        zoff[l] = zbytes;
+        zbytes += round_up(T * round_up((size_t)L->r, 8) * 2, 256);
+    }
+    void* z = dev_alloc(zbytes);
+    H->z.push_back(z);
+    std::vector<WmSpec> s1, s2;
+    for (size_t l = 0; l < nlin; ++l) {
+        const pg_layer L = Ls[l];
+        const int rp = (int)round_up((size_t)L->r, 8);
+        void* zl = static_cast<char*>(z) + zoff[l];
+        s1.push_back(WmSpec{L->bt, L->ldb, L->r, L->n, x, L->n, zl, rp, 1, masks[l], (long long)sel_mask_ld(L->r)});
+        s2.push_back(WmSpec{L->a, L->lda, L->m, L->r, zl, rp, ys[l], L->m, ydt == PG_BF16 ? 1 : 0});
+    }
+    H->prog->add_phase(s1);
+    H->prog->add_phase(s2);
+    PG_API_END
+}
+
+int pg_union_prog_run(pg_union_prog H, const int32_t* tok_pat, pg_stream s) {
+    PG_API_BEGIN
+    require(H && tok_pat, PG_INVALID_ARGUMENT, "union_prog_run: bad arguments");
+    H->prog->run(tok_pat, as_stream(s));
+    PG_API_END
+}
+
+int pg_union_prog_info(pg_union_prog H, size_t* phases, size_t* grid) {
+    PG_API_BEGIN
+    require(H, PG_INVALID_ARGUMENT, "union_prog_info: bad arguments");
+    if (phases) *phases = (size_t)H->prog->phases();
+    if (grid) *grid = (size_t)H->prog->grid();
+    PG_API_END
+}
+
+int pg_union_prog_debug(pg_union_prog H, uint64_t* out, size_t n, int* have) {
+    PG_API_BEGIN
+    require(H && out && have, PG_INVALID_ARGUMENT, "union_prog_debug: bad arguments");
+    PG_CUDA_THROW(cudaDeviceSynchronize());
+    *have = H->prog->debug_dump(reinterpret_cast<unsigned long long*>(out), n);
+    PG_API_END
+}
+
+int pg_union_prog_destroy(pg_union_prog H) {
+    PG_API_BEGIN
+    delete H;
     PG_API_END
 }
 
