@@ -234,43 +234,54 @@ def config4_arm(args, rank, world, local_rank):
     stack, ldims = build_stack(pg, torch, dev, prompts, args.layers)
     tp = torch.arange(Pl, device=dev, dtype=torch.int32)  # token t -> its prompt's selection t
     g = torch.Generator(device=dev).manual_seed(5)
-    buf = {"x": torch.randn(Pl, D_MODEL, device=dev, generator=g).to(torch.bfloat16)}
-    for nm, (m, n) in LIN.items():
-        buf[nm] = torch.empty(Pl, m, device=dev, dtype=torch.bfloat16)
-    x_host = torch.empty(Pl, D_MODEL, dtype=torch.bfloat16).pin_memory()
-    x_host.copy_(buf["x"].cpu())
-    y_host = torch.empty(Pl, D_MODEL, dtype=torch.bfloat16).pin_memory()
-
-    def layer(lay, first):
+    x0 = torch.randn(Pl, D_MODEL, device=dev, generator=g).to(torch.bfloat16)
+    # the whole step as ONE persistent launch (union_prog.cu): per-layer
+    # activation buffers (a program writes each buffer once), layer l+1 reads
+    # layer l's output tile by tile
+    prog = pg.UnionProgram(Pl)
+    bufs = []
+    src = x0
+    for lay in stack:
+        b = {"x": src}
         for grp in GROUPS:
-            src = SRC[grp[0]]
-            if src == "x" and not first:
-                src = "down"  # layer l+1 reads layer l's output
-            pg.module_forward_union([lay[n][0] for n in grp], [lay[n][1] for n in grp], tp, buf[src],
-                                    out_dtype=torch.bfloat16, outs=[buf[n] for n in grp])
+            for nm in grp:
+                b[nm] = torch.empty(Pl, LIN[nm][0], device=dev, dtype=torch.bfloat16)
+            prog.add_module([lay[nm][0] for nm in grp], [lay[nm][1] for nm in grp], b[SRC[grp[0]]],
+                            [b[nm] for nm in grp])
+        bufs.append(b)
+        src = b["down"]
+    y_dev = bufs[-1]["down"]
+    x_host = torch.empty(Pl, D_MODEL, dtype=torch.bfloat16).pin_memory()
+    x_host.copy_(x0.cpu())
+    y_host = torch.empty(Pl, D_MODEL, dtype=torch.bfloat16).pin_memory()
 
     def step(host_io):
         if host_io:
-            pg.copy_io(buf["x"], x_host)     # the step's input hidden states, H2D
-        for li, lay in enumerate(stack):
-            layer(lay, li == 0)
+            pg.copy_io(x0, x_host)      # the step's input hidden states, H2D
+        prog.run(tp)
         if host_io:
-            pg.copy_io(y_host, buf["down"])  # the last layer's output, D2H
+            pg.copy_io(y_host, y_dev)   # the last layer's output, D2H
+
+    def modules():  # the same step as per-module launches (2 union GEMM launches per module)
+        for lay, b in zip(stack, bufs):
+            for grp in GROUPS:
+                pg.module_forward_union([lay[n][0] for n in grp], [lay[n][1] for n in grp], tp, b[SRC[grp[0]]],
+                                        out_dtype=torch.bfloat16, outs=[b[n] for n in grp])
 
     st = torch.cuda.Stream(device=dev)
     graphs = {}
-    for host_io in (False, True):
+    for key, fn in ((False, lambda: step(False)), (True, lambda: step(True)), ("modules", modules)):
         with torch.cuda.stream(st):
-            step(host_io)  # sizes workspaces / pools outside capture
+            fn()  # sizes workspaces / pools outside capture
         st.synchronize()
         gr = torch.cuda.CUDAGraph()
         n0 = pg.launch_count()
         with torch.cuda.graph(gr, stream=st):
-            step(host_io)
-        graphs[host_io] = (gr, pg.launch_count() - n0)
+            fn()
+        graphs[key] = (gr, pg.launch_count() - n0)
 
-    def timed(host_io, steps, warmup):
-        gr = graphs[host_io][0]
+    def timed(key, steps, warmup):
+        gr = graphs[key][0]
         with torch.cuda.stream(st):
             for _ in range(warmup):
                 gr.replay()
@@ -289,30 +300,18 @@ def config4_arm(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ms_total, ms_med = timed(False, args.steps, args.warmup)
     ms_e2e, ms_e2e_med = timed(True, args.steps, max(1, args.warmup // 2))
+    _, ms_modules = timed("modules", min(args.steps, 10), 2)
     launches = graphs[False][1]
-
-    # dominant module: up+gate (both union GEMM stages, 2 launches, 144 MB of
-    # stored experts: 36 % of the layer's bytes), timed alone with CUDA events
-    lay0 = stack[0]
-    dom_bytes = sum(lay0[nm][0].r_store * (LIN[nm][0] + LIN[nm][1]) * 2 for nm in ("up", "gate"))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    def ug():
-        pg.module_forward_union([lay0["up"][0], lay0["gate"][0]], [lay0["up"][1], lay0["gate"][1]], tp, buf["o"],
-                                out_dtype=torch.bfloat16, outs=[buf["up"], buf["gate"]])
-
+    # the modules path and the program must agree (the same step, two schedules)
     with torch.cuda.stream(st):
-        for _ in range(3):
-            ug()
-        e0.record(st)
-        for _ in range(10):
-            ug()
-        e1.record(st)
+        graphs["modules"][0].replay()
+        ref = y_dev.float().clone()
+        graphs[False][0].replay()
     st.synchronize()
-    dom_us = e0.elapsed_time(e1) / 10 * 1e3
-    dom = {"what": "up+gate module alone (union GEMM stages 1 and 2, 2 launches), eager, CUDA events",
-           "alg_bytes": dom_bytes, "us": dom_us, "achieved_gbs": dom_bytes / (dom_us * 1e-6) / 1e9,
-           "frac": dom_bytes / (dom_us * 1e-6) / 1e9 / hbm_peak}
+    agree = float((y_dev.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+    dom = {"what": "k_union_prog: the whole step (all 32 x 8 union GEMM stages) is one launch",
+           "modules_ms_per_step": ms_modules, "modules_launches_per_step": graphs["modules"][1],
+           "program_vs_modules_rel": agree}
 
     bytes_step = args.layers * sum(ldims[i][0] * (m + n) * 2 for i, (m, n) in enumerate(LIN.values()))
     flops_step = args.layers * 2 * Pl * sum(ldims[i][0] * (m + n) for i, (m, n) in enumerate(LIN.values()))
@@ -331,7 +330,8 @@ def config4_arm(args, rank, world, local_rank):
         "config": {"workload": f"config4: {args.layers}-layer LLaMA-7B-shaped stack of rank-expert linears "
                                f"(q/k/v/o 4096x4096, gate/up 4096->11008, down 11008->4096) ratio {RATIO}, decode "
                                f"batch of {Pl} heterogeneous prompts per GPU, each with its own expert subset per "
-                               f"linear (union-masked tcgen05 GEMMs, q/k/v and up/gate grouped per stage)",
+                               f"linear (union-masked tcgen05 GEMMs, q/k/v and up/gate grouped per stage, the "
+                               f"whole step one persistent launch: k_union_prog)",
                    "global_batch": glob_tok, "prompts_per_gpu": Pl, "layers": args.layers,
                    "parallelism": f"dp{world} ({args.scaling} scaling; replicated weights, no collective)",
                    "l2": f"{args.layers} distinct layer weight sets, {bytes_step / 1e9:.2f} GB streamed per step "
@@ -343,15 +343,15 @@ def config4_arm(args, rank, world, local_rank):
                       "timed step (pg_copy_io kernels)", "median_ms_per_step": ms_e2e_med},
         "roofline": {"bound": "hbm", "achieved": bytes_step / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                      "frac": bytes_step / step_s / 1e9 / hbm_peak, "traffic": traffic,
-                     "kernel": "the step's union GEMMs (k_union_wm / k_umma_grouped2, 8 per layer): stored expert "
-                               "bytes r_store(m+n)*2 of every linear, read once per step for the whole batch",
+                     "kernel": "k_union_prog (the step's 256 union GEMM stages in one persistent launch): stored "
+                               "expert bytes r_store(m+n)*2 of every linear, read once per step for the whole batch",
                      "alg_bytes_per_step": bytes_step, "tensor_tflops": flops_step / step_s / 1e12,
                      "peak_kind": peak_kind, "dominant_launch": dom},
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "clocks": clk.summary(),
     }
-    del stack, buf
+    del stack, bufs, prog, graphs
     torch.cuda.empty_cache()
     return out
 

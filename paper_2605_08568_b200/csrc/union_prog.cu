@@ -18,12 +18,11 @@
 //   * the weight tiles never depend on activations: a dedicated producer
 //     warp streams them into the ring as soon as a slot is free, across
 //     phase and layer boundaries, while the token producer waits for data;
-//   * split tiles publish f32 partials (tagged flags, per phase) and their
-//     participants reduce one token slice each, in pair order (deterministic),
-//     pulling the partial slices into shared memory with bulk copies (3 x 16 KB
-//     in flight); the partial buffers alternate between two sets by phase
-//     parity and a writer waits until every reader of the slot's previous use
-//     has counted itself out (consumed counters);
+//   * split tiles publish f32 partials (bulk stores from shared-memory
+//     staging, tagged flags per phase) and their participants reduce one token
+//     slice each, in pair order (deterministic); the partial buffers alternate
+//     between two sets by phase parity and a writer waits until every reader of
+//     the slot's previous use has counted itself out (consumed counters);
 //   * the schedule (which pieces a pair runs, in order) is computed on the host
 //     into one 128-byte record per piece, so no role walks phase metadata with
 //     dependent global loads on the critical path.
@@ -51,19 +50,20 @@
 
 namespace pg {
 
-constexpr int UP_STAGES = 5;
+#ifndef UP_STAGES_CFG
+#define UP_STAGES_CFG 6
+#endif
+constexpr int UP_STAGES = UP_STAGES_CFG;
 constexpr int UP_STAGE_BYTES = WM_W_BYTES + WM_X_BYTES;  // 32 KB
 constexpr int UP_THREADS = 224;
 constexpr int UP_MAXG = 4;
 constexpr int UP_POLL_NS = 100;  // back-off between polls of a dependency counter
 constexpr int UP_CSTRIDE = 32;   // ready counters one per 128-byte line
 constexpr int UP_RED_UNROLL = 3;  // LSU reduction: participants' loads in flight per batch
-constexpr int UP_RED_SLOTS = 3;                                 // reduction bulk-copy slots
-constexpr int UP_RED_SLOT_BYTES = 32 * WM_BM * 4;               // 32 tokens x 128 rows f32 = 16 KB
-constexpr int UP_RED_BYTES = UP_RED_SLOTS * UP_RED_SLOT_BYTES;  // 48 KB (aliases the epilogue staging)
-static_assert(UP_RED_BYTES >= 4 * WM_STG_BYTES, "staging must fit in the reduction buffer");
-// [align slack][ring][barriers + slots, 1 KB][token -> pattern table, 1 KB][reduction buffer / staging]
-constexpr int UP_SMEM = 1024 + UP_STAGES * UP_STAGE_BYTES + 1024 + WM_TMAX * 4 + UP_RED_BYTES;
+constexpr int UP_STG_BYTES = 2 * 32 * WM_BM * 4;  // epilogue staging: 2 x [32 tokens][128 rows] f32 (partial drain)
+static_assert(UP_STG_BYTES >= 4 * WM_STG_BYTES, "whole-tile staging must fit");
+// [align slack][ring][barriers + slots, 1 KB][token -> pattern table, 1 KB][epilogue staging]
+constexpr int UP_SMEM = 1024 + UP_STAGES * UP_STAGE_BYTES + 1024 + WM_TMAX * 4 + UP_STG_BYTES;
 
 struct __align__(64) UpGroup {
     CUtensorMap wmap;  // weights [R, K], box {64, 128}
@@ -98,7 +98,6 @@ struct UpParams {
     float* partial;            // [2][pairs][2][WM_PART_FLOATS]
     unsigned long long* epoch;
     unsigned long long* dbg;
-    int mode;  // bit 0: split-tile partials drained with bulk stores; bit 1: reduction with LSU loads
 };
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
@@ -172,10 +171,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
     uint64_t* empty = bars + UP_STAGES;           // [STAGES] (each CTA)
     uint64_t* tfull = bars + 2 * UP_STAGES;       // [2] (each CTA)
     uint64_t* tempty = bars + 2 * UP_STAGES + 2;  // [2] (leader's copy: both CTAs' epilogues)
-    uint64_t* rbar = bars + 2 * UP_STAGES + 4;    // [UP_RED_SLOTS] reduction bulk copies (each CTA)
-    uint32_t* slots = reinterpret_cast<uint32_t*>(bars + 2 * UP_STAGES + 4 + UP_RED_SLOTS);  // tmem, tag
+    uint32_t* slots = reinterpret_cast<uint32_t*>(bars + 2 * UP_STAGES + 4);  // [0] tmem base, [1] launch tag
     int32_t* tps = reinterpret_cast<int32_t*>(base + UP_STAGES * UP_STAGE_BYTES + 1024);
-    unsigned char* red = base + UP_STAGES * UP_STAGE_BYTES + 1024 + WM_TMAX * 4;
+    unsigned char* stage = base + UP_STAGES * UP_STAGE_BYTES + 1024 + WM_TMAX * 4;  // epilogue staging
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -192,7 +190,6 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             u_mbar_init(u_smem(&tfull[a]), 1);
             u_mbar_init(u_smem(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
         }
-        for (int a = 0; a < UP_RED_SLOTS; ++a) u_mbar_init(u_smem(&rbar[a]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // launch ticket before launch_dependents: every CTA of this launch holds
         // its ticket before a CTA of the next launch can start (old / grid = index)
@@ -300,14 +297,13 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
         // ------------------------------------------------ epilogue (warps 3-6, both CTAs)
         const int et = threadIdx.x - 96;  // 0..127
         const int q = warp & 3;
-        float* stg = reinterpret_cast<float*>(red) + q * (WM_STG_BYTES / 4);
+        float* stg = reinterpret_cast<float*>(stage) + q * (WM_STG_BYTES / 4);
         asm volatile("griddepcontrol.wait;" ::: "memory");  // outputs may still be read by the previous kernel
         for (int t = et; t < P.T; t += 128) tps[t] = P.tok_pat ? __ldg(P.tok_pat + t) : 0;
         // reads of this pair's partial slots per launch, per parity set: a writer
         // waits for all readers of the slot's previous use before reusing it
         const unsigned tot[2] = {P.pair_tot[pair * 2], P.pair_tot[pair * 2 + 1]};
         unsigned used[2] = {0u, 0u};
-        uint32_t rph = 0;  // reduction slot parities (bit per slot)
         wm_bar_epi();
         int acc = 0, pi = 0, lastf = -1;
         uint32_t aph = 0;
@@ -330,12 +326,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             if (!R.split) {
                 const UpOut G{R.out, R.ldo, R.out_bf16, R.mask, R.mask_ld, R.Rs};
                 wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps, stg, lane);
-            } else if (P.mode & 1) {
-                up_epi_partial_bulk(P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
-                                    reinterpret_cast<float*>(red), lane, et);
             } else {
-                wm_epi_partial(P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
-                               stg, lane);
+                up_epi_partial_bulk(P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
+                                    reinterpret_cast<float*>(stage), lane, et);
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -358,8 +351,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             if (!R.last_in_phase) continue;
             if (red_rec >= 0) {
                 // ---- this pair's token slice of its split tile: the n partials'
-                // slices pulled into shared memory (bulk copies, 3 x 16 KB in
-                // flight), summed in pair order (deterministic), masked, stored
+                // slices loaded (LSU, three participants in flight), summed in pair
+                // order (deterministic), masked, stored
                 const UpRec& S = P.recs[red_rec];
                 const int pf = S.pf, n = S.n, me = pair - pf;
                 void* const sout = S.out;
@@ -367,7 +360,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 const long long sldo = S.ldo, smask_ld = S.mask_ld;
                 const int sRs = S.Rs, sbf16 = S.out_bf16, sflags = S.flag_base, sready = S.ready_idx;
                 const int row0 = S.row0 + (int)rank * WM_BM;
-                const int ta = me * P.Tp / n, tb = min(P.T, (me + 1) * P.Tp / n);
+                // token slice of this participant, 4-aligned (float4 along tokens)
+                const int ta = me * (P.Tp / 4) / n * 4, tb = min(P.T, (me + 1) * (P.Tp / 4) / n * 4);
                 const int cnt = max(0, tb - ta);
                 if (warp == 3)  // every participant's flag, one lane each
                     for (int pp = pf + lane; pp < pf + n; pp += 32) {
@@ -417,7 +411,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                         }
                     }
                 };
-                if (P.mode & 2) {
+                {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     // LSU: per 32-token chunk, 8 float4 per thread per participant,
                     // three participants' loads in flight at a time, summed in pair order
@@ -446,55 +440,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                         }
                         store_chunk(ch, ct, F4x8{a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]});
                     }
-                } else {
-                const int C = (cnt + 31) / 32 * n;  // copies: (32-token chunk, participant), participant fastest
-                auto issue = [&](int c) {
-                    const int ch = c / n, pp = c % n, t0 = ta + ch * 32, ct = min(32, tb - t0);
-                    const uint32_t bytes = (uint32_t)ct * WM_BM * 4;
-                    const uint32_t sb = u_smem(&rbar[c % UP_RED_SLOTS]);
-                    u_mbar_arrive_tx(sb, bytes);
-                    bulk_g2s(u_smem(red + (c % UP_RED_SLOTS) * UP_RED_SLOT_BYTES),
-                             pbase + (size_t)(pf + pp) * 2 * WM_PART_FLOATS + (size_t)t0 * WM_BM, bytes, sb);
-                };
-                if (et == 0 && C > 0) {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    for (int c = 0; c < min(C, UP_RED_SLOTS); ++c) issue(c);
-                }
-                // a thread owns float4 e = et + 128 j (j < 8) of a 32-token chunk:
-                // token e / 32, rows 4 (e % 32) .. + 3
-                float4 a[8];
-                for (int c = 0; c < C; ++c) {
-                    const int ch = c / n, pp = c % n, slot = c % UP_RED_SLOTS;
-                    const int ct = min(32, tb - (ta + ch * 32));
-                    u_mbar_wait(u_smem(&rbar[slot]), (rph >> slot) & 1u);
-                    rph ^= 1u << slot;
-                    if (et == 0 && f == 0) {
-                        if (c == 0) UP_STAMP(57);
-                        if (c == 1) UP_STAMP(58);
-                        if (c == C - 1) UP_STAMP(59);
-                    }
-                    const float4* sp = reinterpret_cast<const float4*>(red + slot * UP_RED_SLOT_BYTES);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int e = et + 128 * j;
-                        if ((e >> 5) < ct) {
-                            const float4 v = sp[e];
-                            if (pp == 0) {
-                                a[j] = v;
-                            } else {
-                                a[j].x += v.x; a[j].y += v.y; a[j].z += v.z; a[j].w += v.w;
-                            }
-                        }
-                    }
-                    wm_bar_epi();  // every thread is done with this slot
-                    if (et == 0 && c + UP_RED_SLOTS < C) issue(c + UP_RED_SLOTS);
-                    if (pp != n - 1) continue;
-                    store_chunk(ch, ct, F4x8{a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]});
-                }
                 }
                 wm_bar_epi();  // slice stored
-                if (et == 0 && f == 0) UP_STAMP(60);
                 if (et == 0) {
                     __threadfence();
                     red_release_add(P.ready + (size_t)(sready + (int)rank) * UP_CSTRIDE, 1u);
@@ -806,8 +753,6 @@ void UnionProgram::finalize(cudaStream_t st) {
     P.consumed = reinterpret_cast<unsigned*>(I.ws + o_cons);
     P.partial = reinterpret_cast<float*>(I.ws + o_part);
     P.dbg = I.dbg;
-    const char* m = getenv("PG_PROG_MODE");
-    P.mode = m ? atoi(m) : 0;
     I.finalized = true;
 }
 
@@ -839,7 +784,7 @@ void UnionProgram::run(const int32_t* tok_pat, cudaStream_t st) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_union_prog, P));
+        PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_union_prog, P));
     count_launch();
 }
 

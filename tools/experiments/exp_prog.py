@@ -87,5 +87,3 @@ if os.environ.get("PG_PROG_DBG"):
     print("phase  W_first      X_first      X_last       epi_p0       epi_all      flags        done   (med/max us)")
     for f in range(8):
         print(f"{names[f]:5s} " + " ".join(col(k) for k in (49 + f, 33 + f, 41 + f, 1 + f, 9 + f, 17 + f, 25 + f)))
-    print("qkv1 reduction: first copy", col(57), "second", col(58), "last", col(59), "stored", col(60),
-          )
