@@ -699,7 +699,7 @@ def main():
         if rank != 0:
             return
         ref = reference_config4(repeats=max(1, min(args.steps, 3)))
-        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": 0, "steps": args.steps,
+        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": N_PROMPTS / ref["value"] * 1e3,
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",

@@ -14,6 +14,8 @@ import ctypes as C
 import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libparse_gpu.so")
+if os.environ.get("PG_LIB_VARIANT"):  # experiments only: lib/libparse_gpu_<variant>.so (tools/experiments)
+    LIB_PATH = LIB_PATH[:-3] + "_" + os.environ["PG_LIB_VARIANT"] + ".so"
 
 PG_F64, PG_F32, PG_BF16 = 0, 1, 2
 PG_FEATURE_MAJOR, PG_TOKEN_MAJOR = 0, 1

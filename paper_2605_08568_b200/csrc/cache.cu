@@ -214,12 +214,9 @@ __global__ void k_embed_finish(double* __restrict__ h, int d, int* __restrict__ 
 
 void launch_cosine_scan(const double* emb, const double* q, int N, int d, double* sim, double* bnd,
                         cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_cosine_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           200 * 1024));
-        attr = true;
-    }
+    once_per_device(reinterpret_cast<const void*>(&k_cosine_scan), [] {
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_cosine_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    });
     int blocks = min((N + kCosWarps - 1) / kCosWarps, kNumSMs * 2);
     k_cosine_scan<<<blocks, kCosWarps * 32, (size_t)d * 8, st>>>(emb, q, N, d, sim, bnd);
     PG_LAUNCH_CHECK();

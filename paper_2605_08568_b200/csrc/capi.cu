@@ -66,12 +66,9 @@ void launch_transpose(pg_dtype dt, const void* src, int rows, int cols, void* ds
 
 // ---- stream-ordered scratch (freed when the scope ends, after queued work) ----
 static void init_pool() {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return;
+    once_per_device(reinterpret_cast<const void*>(&init_pool), [] {
         cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }

@@ -775,23 +775,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     STAMP(13);
 }
 
-static int g_num_sms = 0;
-int chain_grid() {
-    if (!g_num_sms) {
-        int dev = 0;
-        PG_CUDA_THROW(cudaGetDevice(&dev));
-        PG_CUDA_THROW(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return g_num_sms;
-}
+int chain_grid() { return device_sms(); }
 
 template <typename W, bool PEER>
 static void launch_chain_t(const ChainParams& P, size_t smem, cudaStream_t st, int grid) {
-    static bool attr = false;
-    if (!attr) {
+    once_per_device(reinterpret_cast<const void*>(&k_chain<W, PEER>), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_chain<W, PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid > 0 ? std::min(grid, chain_grid()) : chain_grid());
     cfg.blockDim = dim3(kChainThreads);

@@ -86,7 +86,40 @@ __global__ void k_fill_normal(T* out, size_t count, uint64_t seed, double scale)
 
 }  // namespace
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace pg {
+
+int current_device() {
+    int dev = 0;
+    PG_CUDA_THROW(cudaGetDevice(&dev));
+    return dev;
+}
+
+int device_sms() {
+    static std::atomic<int> sms[128];
+    const int dev = current_device();
+    if (dev < 0 || dev >= 128) throw Error{PG_CUDA_ERROR, "device index out of range"};
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (!v) {
+        PG_CUDA_THROW(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        sms[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+void once_per_device(const void* tag, void (*fn)()) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({tag, dev})) return;
+    fn();
+    done.insert({tag, dev});
+}
+
 void launch_fill_normal(void* out, pg_dtype dt, size_t count, uint64_t seed, double scale,
                         cudaStream_t st) {
     const int blocks = kNumSMs * 8;

@@ -40,6 +40,13 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
             throw ::pg::Error{PG_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(_e)}; \
     } while (0)
 
+// ---- per-device host state (one process may drive several GPUs) ----
+int current_device();
+int device_sms();  // SM count of the current device (cached per device)
+// Runs fn() once per device (under a lock; later callers on that device wait
+// for it): kernel attributes, pool settings.  `tag` identifies the call site.
+void once_per_device(const void* tag, void (*fn)());
+
 inline cudaStream_t as_stream(pg_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline size_t dtype_size(pg_dtype d) { return d == PG_F64 ? 8 : d == PG_F32 ? 4 : 2; }

@@ -521,13 +521,10 @@ static size_t sel_smem(int r, bool band) {
 }
 
 void select_smem_setup() {
-    static bool done = false;
-    if (done) return;
-    PG_CUDA_THROW(cudaFuncSetAttribute(k_select_topk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
-    PG_CUDA_THROW(cudaFuncSetAttribute(k_route_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       200 * 1024));
-    done = true;
+    once_per_device(reinterpret_cast<const void*>(&k_select_topk), [] {
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_select_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_route_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    });
 }
 
 int max_select_rows() { return (200 * 1024 - 64) / 13; }

@@ -681,22 +681,18 @@ static int umma_pairs_enabled() {
 }
 
 void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    once_per_device(reinterpret_cast<const void*>(&k_umma_grouped), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    });
     // CTA pairs for batches whose every GEMM has at least 256 rows
     bool pairs = umma_pairs_enabled() != 0;
     for (const UmmaSpec& sp : specs)  // (+ 16-byte aligned output rows for the TMA-store epilogue)
         pairs = pairs && sp.M >= 2 * UM_BM && (sp.ldo * (sp.out_bf16 ? 2 : 4)) % 16 == 0 &&
                 reinterpret_cast<uintptr_t>(sp.out) % 16 == 0;
-    int dev = 0, sms = 0;
-    PG_CUDA_THROW(cudaGetDevice(&dev));
-    PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int sms = device_sms();
     for (size_t g0 = 0; g0 < specs.size(); g0 += UM_MAX_GROUPS) {
         const int ng = (int)std::min<size_t>(UM_MAX_GROUPS, specs.size() - g0);
         auto P = std::make_unique<UmmaParams>();
@@ -897,9 +893,7 @@ static int splitk_plan(const UmmaSpec& s, int* bn_out, int* kslice_out) {
         const char* e = getenv("PG_UMMA_SPLITK");  // max K slices (1 disables)
         return e ? std::max(1, atoi(e)) : UM_MAX_GROUPS;
     }();
-    int dev = 0, sms = 0;
-    PG_CUDA_THROW(cudaGetDevice(&dev));
-    PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int sms = device_sms();
     const bool pairs = umma_pairs_enabled() != 0 && s.M >= 2 * UM_BM;
     const int rows = pairs ? 2 * UM_BM : UM_BM, slots = pairs ? sms / 2 : sms;
     int bn = pick_bn(s.N);
@@ -966,9 +960,7 @@ bool launch_umma_splitk_multi(const std::vector<UmmaSpec>& specs, void* ws, cuda
         w += (size_t)Ss[j] * s.M * s.N;
     }
     launch_umma(parts, st);
-    int dev = 0, sms = 0;
-    PG_CUDA_THROW(cudaGetDevice(&dev));
-    PG_CUDA_THROW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int sms = device_sms();
     for (size_t j = 0; j < specs.size(); ++j) {
         const UmmaSpec& s = specs[j];
         const long long n4 = (long long)s.M * s.N / 4;

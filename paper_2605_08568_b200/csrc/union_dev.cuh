@@ -55,7 +55,7 @@ constexpr int WM_STG_BYTES = 32 * 32 * 4;
 // whole tile: TMEM -> smem transpose -> (mask) -> Y[t, row0 .. row0 + 31]
 template <class G_>
 __device__ __forceinline__ void wm_epi_direct(int Tp, int T, const G_& G, uint32_t taddr, int row0,
-                                              const int32_t* tps, float* stg, int lane) {
+                                              const int32_t* tps, float* stg, int lane, int c0 = 0, int cstep = 1) {
     const int nch = Tp / 32;
     void* const out = G.out;
     const long long ldo = G.ldo;
@@ -64,7 +64,7 @@ __device__ __forceinline__ void wm_epi_direct(int Tp, int T, const G_& G, uint32
     const long long mask_ld = G.mask_ld;
     const int R = G.Rs;
     uint32_t ra[32];
-    for (int c = 0; c < nch; ++c) {
+    for (int c = c0; c < nch; c += cstep) {
         // this chunk's 4 selection-mask words, loaded before the TMEM read and
         // every store (loads issued after stores would serialise on aliasing)
         uint2 mw[4];

@@ -40,6 +40,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -55,13 +56,19 @@ namespace pg {
 #endif
 constexpr int UP_STAGES = UP_STAGES_CFG;
 constexpr int UP_STAGE_BYTES = WM_W_BYTES + WM_X_BYTES;  // 32 KB
-constexpr int UP_THREADS = 224;
+#ifndef UP_EPI_WARPS_CFG
+#define UP_EPI_WARPS_CFG 8
+#endif
+constexpr int UP_EPI_WARPS = UP_EPI_WARPS_CFG;  // 4 or 8: 1 or 2 warps per TMEM lane quadrant
+constexpr int UP_EPI_T = 32 * UP_EPI_WARPS;
+constexpr int UP_EPI_H = UP_EPI_WARPS / 4;      // epilogue halves (chunk interleave)
+constexpr int UP_THREADS = 96 + UP_EPI_T;
 constexpr int UP_MAXG = 4;
 constexpr int UP_POLL_NS = 100;  // back-off between polls of a dependency counter
 constexpr int UP_CSTRIDE = 32;   // ready counters one per 128-byte line
 constexpr int UP_RED_UNROLL = 3;  // LSU reduction: participants' loads in flight per batch
 constexpr int UP_STG_BYTES = 2 * 32 * WM_BM * 4;  // epilogue staging: 2 x [32 tokens][128 rows] f32 (partial drain)
-static_assert(UP_STG_BYTES >= 4 * WM_STG_BYTES, "whole-tile staging must fit");
+static_assert(UP_STG_BYTES >= UP_EPI_WARPS * WM_STG_BYTES, "whole-tile staging must fit");
 // [align slack][ring][barriers + slots, 1 KB][token -> pattern table, 1 KB][epilogue staging]
 constexpr int UP_SMEM = 1024 + UP_STAGES * UP_STAGE_BYTES + 1024 + WM_TMAX * 4 + UP_STG_BYTES;
 
@@ -108,6 +115,8 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
     while ((int)(ld_acquire(p) - target) < 0) __nanosleep(UP_POLL_NS);
 }
+__device__ __forceinline__ void up_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(UP_EPI_T) : "memory"); }
+__device__ __forceinline__ void up_bar_half(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // PG_PROG_DBG=1: %globaltimer stamps [grid][64] for phases f < 8: [0] start,
@@ -119,39 +128,48 @@ __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefe
         if (P.dbg) P.dbg[blockIdx.x * 64 + (k)] = wm_gtimer();            \
     } while (0)
 
-// split tile: TMEM -> [32 tokens][128 rows] f32 chunk in shared memory (the 4
-// epilogue warps together, 16 KB, double-buffered) -> one 16 KB bulk store per
-// chunk into the partial [Tp][128]; the stores are complete (and ordered before
-// the caller's release) on return.
-__device__ __forceinline__ void up_epi_partial_bulk(int Tp, uint32_t taddr, float* dst, int q, float* buf, int lane,
-                                                    int et) {
+// split tile: TMEM -> [32 tokens][128 rows] f32 chunk in shared memory (4
+// epilogue warps, one per TMEM lane quadrant, 16 KB) -> one 16 KB bulk store
+// per chunk into the partial [Tp][128].  With 8 epilogue warps the two halves
+// take alternate chunks, each with its own staging buffer and named barrier;
+// with 4, one half double-buffers.  The stores are complete (and ordered
+// before the caller's release) on return.
+__device__ __forceinline__ void up_epi_partial_bulk(int Tp, uint32_t taddr, float* dst, int q, int h, float* buf,
+                                                    int lane, int et) {
     const int nch = Tp / 32;
+    const bool lead = (et & 127) == 0;
     uint32_t ra[32];
-    for (int c = 0; c < nch; ++c) {
-        float* b = buf + (c & 1) * (32 * WM_BM);
-        if (et == 0 && c >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        wm_bar_epi();  // buffer c & 1 is free
+    for (int c = h; c < nch; c += UP_EPI_H) {
+        const int bi = UP_EPI_H == 2 ? h : (c & 1);
+        float* b = buf + bi * (32 * WM_BM);
+        if (lead && c >= 2) {
+            if (UP_EPI_H == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+        up_bar_half(h);  // this half's buffer is free
         tmem_ld32(taddr + 32u * c, ra);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) b[j * WM_BM + q * 32 + lane] = __uint_as_float(ra[j]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        wm_bar_epi();  // chunk written
-        if (et == 0) {
+        up_bar_half(h);  // chunk written
+        if (lead) {
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + (size_t)c * 32 * WM_BM),
                          "r"(u_smem(b)), "r"(32 * WM_BM * 4)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
     }
-    if (et == 0) {
+    if (lead) {
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
     }
 }
 
-struct F4x8 {
-    float4 v[8];
+constexpr int UP_RED_E = 32 * 32 / UP_EPI_T;  // float4s of a 32-token chunk per epilogue thread
+struct F4xE {
+    float4 v[UP_RED_E];
 };
 
 struct UpOut {  // epilogue view of a record (wm_epi_direct / wm_put)
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
         }
         for (int a = 0; a < 2; ++a) {
             u_mbar_init(u_smem(&tfull[a]), 1);
-            u_mbar_init(u_smem(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
+            u_mbar_init(u_smem(&tempty[a]), 2 * UP_EPI_WARPS);  // epilogue warps x 2 CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // launch ticket before launch_dependents: every CTA of this launch holds
@@ -295,16 +313,16 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
         }
     } else {
         // ------------------------------------------------ epilogue (warps 3-6, both CTAs)
-        const int et = threadIdx.x - 96;  // 0..127
-        const int q = warp & 3;
-        float* stg = reinterpret_cast<float*>(stage) + q * (WM_STG_BYTES / 4);
+        const int et = threadIdx.x - 96;  // 0 .. UP_EPI_T - 1
+        const int q = warp & 3, h = (warp - 3) >> 2;  // TMEM lane quadrant; half (chunk interleave)
+        float* stg = reinterpret_cast<float*>(stage) + (warp - 3) * (WM_STG_BYTES / 4);
         asm volatile("griddepcontrol.wait;" ::: "memory");  // outputs may still be read by the previous kernel
-        for (int t = et; t < P.T; t += 128) tps[t] = P.tok_pat ? __ldg(P.tok_pat + t) : 0;
+        for (int t = et; t < P.T; t += UP_EPI_T) tps[t] = P.tok_pat ? __ldg(P.tok_pat + t) : 0;
         // reads of this pair's partial slots per launch, per parity set: a writer
         // waits for all readers of the slot's previous use before reusing it
         const unsigned tot[2] = {P.pair_tot[pair * 2], P.pair_tot[pair * 2 + 1]};
         unsigned used[2] = {0u, 0u};
-        wm_bar_epi();
+        up_bar_epi();
         int acc = 0, pi = 0, lastf = -1;
         uint32_t aph = 0;
         int red_rec = -1;  // this pair's split piece of the current phase
@@ -321,19 +339,19 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             }
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (R.split) wm_bar_epi();  // the slot wait above
+            if (R.split) up_bar_epi();  // the slot wait above
             const uint32_t taddr = tmem + (uint32_t)(acc * WM_TMAX) + ((uint32_t)(q * 32) << 16);
             if (!R.split) {
                 const UpOut G{R.out, R.ldo, R.out_bf16, R.mask, R.mask_ld, R.Rs};
-                wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps, stg, lane);
+                wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps, stg, lane, h, UP_EPI_H);
             } else {
                 up_epi_partial_bulk(P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
-                                    reinterpret_cast<float*>(stage), lane, et);
+                                    h, reinterpret_cast<float*>(stage), lane, et);
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
-            wm_bar_epi();  // every epilogue thread's stores are issued (and the staging is free)
+            up_bar_epi();  // every epilogue thread's stores are issued (and the staging is free)
             if (et == 0) {
                 __threadfence();
                 if (R.split) {
@@ -368,24 +386,24 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                         const unsigned* fl = P.flags + sflags + pp * 2 + (int)rank;
                         while (ld_acquire(fl) != tag) __nanosleep(UP_POLL_NS);
                     }
-                wm_bar_epi();
+                up_bar_epi();
                 if (et == 0 && f < 8) UP_STAMP(17 + f);
                 const float* pbase = P.partial + ((size_t)(set * np) * 2 + rank) * WM_PART_FLOATS;
-                auto store_chunk = [&](int ch, int ct, const F4x8& a) {
+                auto store_chunk = [&](int ch, int ct, const F4xE& a) {
                     // chunk complete: masks first (read-only path, all 8 in flight), then
                     // the stores (plain loads after stores would serialise on aliasing)
-                    uint32_t mw[8];
+                    uint32_t mw[UP_RED_E];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int e = et + 128 * j, tl = e >> 5, c4 = e & 31;
+                    for (int j = 0; j < UP_RED_E; ++j) {
+                        const int e = et + UP_EPI_T * j, tl = e >> 5, c4 = e & 31;
                         mw[j] = 0xFFFFFFFFu;
                         if (smask && tl < ct)
                             mw[j] = __ldg(reinterpret_cast<const uint32_t*>(
                                 smask + (long long)tps[ta + ch * 32 + tl] * smask_ld + row0 + 4 * c4));
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int e = et + 128 * j, tl = e >> 5, c4 = e & 31;
+                    for (int j = 0; j < UP_RED_E; ++j) {
+                        const int e = et + UP_EPI_T * j, tl = e >> 5, c4 = e & 31;
                         if (tl >= ct) continue;
                         float4 v = a.v[j];
                         const int tok = ta + ch * 32 + tl, row = row0 + 4 * c4;
@@ -413,35 +431,35 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 };
                 {
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    // LSU: per 32-token chunk, 8 float4 per thread per participant,
+                    // LSU: per 32-token chunk, UP_RED_E float4 per thread per participant,
                     // three participants' loads in flight at a time, summed in pair order
                     for (int ch = 0; ch * 32 < cnt; ++ch) {
                         const int ct = min(32, cnt - ch * 32);
-                        float4 a[8];
+                        F4xE a;
                         for (int pp = 0; pp < n; pp += UP_RED_UNROLL) {
-                            float4 v[UP_RED_UNROLL][8];
+                            float4 v[UP_RED_UNROLL][UP_RED_E];
                             const float* s0 = pbase + (size_t)(pf + pp) * 2 * WM_PART_FLOATS + (size_t)(ta + ch * 32) * WM_BM;
 #pragma unroll
                             for (int u = 0; u < UP_RED_UNROLL; ++u)
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) {
-                                    const int e = et + 128 * j;
+                                for (int j = 0; j < UP_RED_E; ++j) {
+                                    const int e = et + UP_EPI_T * j;
                                     if (pp + u < n && (e >> 5) < ct)
                                         v[u][j] = __ldcg(reinterpret_cast<const float4*>(s0 + (size_t)u * 2 * WM_PART_FLOATS) + e);
                                 }
 #pragma unroll
                             for (int u = 0; u < UP_RED_UNROLL; ++u)
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) {
+                                for (int j = 0; j < UP_RED_E; ++j) {
                                     if (pp + u >= n) continue;
-                                    if (pp + u == 0) a[j] = v[u][j];
-                                    else { a[j].x += v[u][j].x; a[j].y += v[u][j].y; a[j].z += v[u][j].z; a[j].w += v[u][j].w; }
+                                    if (pp + u == 0) a.v[j] = v[u][j];
+                                    else { a.v[j].x += v[u][j].x; a.v[j].y += v[u][j].y; a.v[j].z += v[u][j].z; a.v[j].w += v[u][j].w; }
                                 }
                         }
-                        store_chunk(ch, ct, F4x8{a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]});
+                        store_chunk(ch, ct, a);
                     }
                 }
-                wm_bar_epi();  // slice stored
+                up_bar_epi();  // slice stored
                 if (et == 0) {
                     __threadfence();
                     red_release_add(P.ready + (size_t)(sready + (int)rank) * UP_CSTRIDE, 1u);
@@ -460,28 +478,31 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
 
 // ---------------------------------------------------------------- host side
 namespace {
-int up_max_pairs() {
-    static int v = [] {
+int up_max_pairs() {  // co-resident CTA pairs (per device); sets the smem attribute first
+    static std::atomic<int> cache[128];
+    const int dev = current_device();
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v) return v;
+    once_per_device(reinterpret_cast<const void*>(&k_union_prog), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_union_prog, cudaFuncAttributeMaxDynamicSharedMemorySize, UP_SMEM));
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaLaunchConfig_t q = {};
-        q.gridDim = dim3((unsigned)(sms / 2 * 2));
-        q.blockDim = dim3(UP_THREADS);
-        q.dynamicSmemBytes = UP_SMEM;
-        cudaLaunchAttribute a[1];
-        a[0].id = cudaLaunchAttributeClusterDimension;
-        a[0].val.clusterDim.x = 2;
-        a[0].val.clusterDim.y = 1;
-        a[0].val.clusterDim.z = 1;
-        q.attrs = a;
-        q.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k_union_prog, &q) != cudaSuccess || n <= 0) n = sms / 2;
-        return std::min(n, sms / 2);
-    }();
-    return v;
+    });
+    const int sms = device_sms();
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3((unsigned)(sms / 2 * 2));
+    q.blockDim = dim3(UP_THREADS);
+    q.dynamicSmemBytes = UP_SMEM;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = 2;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    q.attrs = a;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_union_prog, &q) != cudaSuccess || n <= 0) n = sms / 2;
+    n = std::min(n, sms / 2);
+    cache[dev].store(n, std::memory_order_relaxed);
+    return n;
 }
 
 struct HGroup {  // host metadata of one GEMM

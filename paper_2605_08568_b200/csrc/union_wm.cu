@@ -41,6 +41,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -398,28 +399,35 @@ std::mutex g_wm_mu;
 // launch tags, so nothing is reset between launches (graph replays included)
 std::map<std::tuple<int, cudaStream_t, int>, WmWorkspace> g_wm_ws;
 
-int wm_max_pairs() {
-    static int v = [] {
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaLaunchConfig_t q = {};
-        q.gridDim = dim3((unsigned)(sms / 2 * 2));
-        q.blockDim = dim3(WM_THREADS);
-        q.dynamicSmemBytes = WM_SMEM;
-        cudaLaunchAttribute a[1];
-        a[0].id = cudaLaunchAttributeClusterDimension;
-        a[0].val.clusterDim.x = 2;
-        a[0].val.clusterDim.y = 1;
-        a[0].val.clusterDim.z = 1;
-        q.attrs = a;
-        q.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k_union_wm, &q) != cudaSuccess || n <= 0) n = sms / 2;
-        if (getenv("PG_UMMA_DEBUG")) fprintf(stderr, "union_wm: max active clusters %d (sms %d)\n", n, sms);
-        return n;
-    }();
-    return v;
+void wm_set_attr() {
+    once_per_device(reinterpret_cast<const void*>(&k_union_wm), [] {
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_union_wm, cudaFuncAttributeMaxDynamicSharedMemorySize, WM_SMEM));
+    });
+}
+
+int wm_max_pairs() {  // co-resident CTA pairs (per device)
+    static std::atomic<int> cache[128];
+    const int dev = current_device();
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v) return v;
+    wm_set_attr();
+    const int sms = device_sms();
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3((unsigned)(sms / 2 * 2));
+    q.blockDim = dim3(WM_THREADS);
+    q.dynamicSmemBytes = WM_SMEM;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = 2;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    q.attrs = a;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_union_wm, &q) != cudaSuccess || n <= 0) n = sms / 2;
+    if (getenv("PG_UMMA_DEBUG")) fprintf(stderr, "union_wm: max active clusters %d (sms %d)\n", n, sms);
+    cache[dev].store(n, std::memory_order_relaxed);
+    return n;
 }
 }  // namespace
 
@@ -475,10 +483,7 @@ bool union_wm_ok(int T, const std::vector<WmSpec>& specs) {
 }
 
 void launch_union_wm(const std::vector<WmSpec>& specs, int T, const int32_t* tok_pat, cudaStream_t st) {
-    static std::once_flag attr;
-    std::call_once(attr, [] {
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_union_wm, cudaFuncAttributeMaxDynamicSharedMemorySize, WM_SMEM));
-    });
+    wm_set_attr();
     if (!union_wm_ok(T, specs)) throw Error{PG_INVALID_ARGUMENT, "union_wm: unsupported batch"};
     const int Tp = (T + 31) / 32 * 32;
     auto P = std::make_unique<WmParams>();

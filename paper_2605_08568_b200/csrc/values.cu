@@ -540,12 +540,9 @@ template <typename W, int TM>
 static void stage1_t(const W* bt, int64_t ldb, SlotMap sm, int nslots, int n, const W* x, int fm,
                      int T, typename Acc<W>::type* z, cudaStream_t st) {
     const size_t smem = (size_t)T * ((n + Vec<W>::n - 1) / Vec<W>::n * Vec<W>::n) * sizeof(W) + 16;
-    static bool attr = false;
-    if (!attr) {
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_stage1_gemv<W, TM>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
+    once_per_device(reinterpret_cast<const void*>(&k_stage1_gemv<W, TM>), [] {
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_stage1_gemv<W, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    });
     const int blocks = min((nslots + 7) / 8, kNumSMs * 4);
     k_stage1_gemv<W, TM><<<blocks, 256, smem, st>>>(bt, ldb, sm, nslots, n, x, fm, T, z);
     PG_LAUNCH_CHECK();
@@ -556,14 +553,12 @@ static void stage2_t(const W* a, int64_t lda, SlotMap sm, int nslots, int m,
                      const typename Acc<W>::type* z, int T, int fm_out, OutT* y, cudaStream_t st) {
     using A = typename Acc<W>::type;
     const size_t smem = (size_t)nslots * T * sizeof(A) + 16;
-    static bool attr = false;
-    if (!attr) {
+    once_per_device(reinterpret_cast<const void*>(&k_stage2_gemv<W, OutT, TM, true>), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_stage2_gemv<W, OutT, TM, true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_stage2_gemv<W, OutT, TM, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
+    });
     const int blocks = min((m + 7) / 8, kNumSMs * 4);
     if (sm.idx)
         k_stage2_gemv<W, OutT, TM, true><<<blocks, 256, smem, st>>>(a, lda, sm, nslots, m, z, T, fm_out, y);

@@ -1,7 +1,7 @@
 """Debug: config-3 down-shape prefill error vs f64/fp32 references."""
 import os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2605_08568_b200 as pg
 m, n = int(os.environ.get("M", 4096)), int(os.environ.get("N", 11008)); P, T = 4, 2048
 K = pg.single_layer_k(m, n, 0.6); r = pg.store_rank(K, min(m, n))

@@ -1,13 +1,13 @@
 """Decode-chain experiment driver (timing only, no parity): MLP block decode
 step with R weight replicas, optional prefetch, fused vs unfused, single
-linear.  Usage: python tools/exp_decode.py [replicas] [steps]"""
+linear.  Usage: python tools/experiments/exp_decode.py [replicas] [steps]"""
 import os
 import sys
 import time
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2605_08568_b200 as pg  # noqa: E402
 import bench  # noqa: E402
 

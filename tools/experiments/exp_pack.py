@@ -1,7 +1,7 @@
 """Device pack timing (config-3 shapes): pack_selected for the 7 linears of a layer, 16 prompts."""
 import os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2605_08568_b200 as pg  # noqa: E402
 LIN = {"q": (4096, 4096), "k": (4096, 4096), "v": (4096, 4096), "o": (4096, 4096),
        "up": (11008, 4096), "gate": (11008, 4096), "down": (4096, 11008)}

@@ -6,7 +6,7 @@ import time
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2605_08568_b200 as pg  # noqa: E402
 
 D, FF, RATIO, P, T = 4096, 11008, 0.6, 16, 2048

@@ -1,7 +1,7 @@
 """Debug: which union path runs, and per-linear device time (q shape, T=256)."""
 import os, sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2605_08568_b200 as pg  # noqa: E402
 from oracle import pyoracle  # noqa: E402
 m, n = int(os.environ.get("M", 4096)), int(os.environ.get("N", 4096))
