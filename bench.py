@@ -673,6 +673,37 @@ def config1_arm(args, local_rank, cpu: bool):
 
 # ======================================================================= main
 
+def dry_run(args, rank, world):
+    """The multi-process plumbing of a --gpus N run without a GPU (CPU tests):
+    one process per rank, a gloo group, this rank's share of the config-4
+    prompts (weak: 256 per rank; strong: 256 split by pattern affinity), a
+    barrier and the max-over-ranks reduction the timed region uses."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_08568_b200 import dist as pgd
+    if world > 1:
+        dist.init_process_group("gloo")
+    prompts = (pgd.partition_by_pattern(list(range(N_PROMPTS)), world)[rank] if args.scaling == "strong"
+               else list(range(N_PROMPTS)))
+    t = 1.0 + rank  # stand-in per-rank time: the line must carry the slowest rank's
+    tmax = max_over_ranks(torch, t, torch.device("cpu"), world)
+    counts = [len(prompts)]
+    if world > 1:
+        buf = [None] * world
+        dist.all_gather_object(buf, prompts)
+        counts = [len(b) for b in buf]
+        covered = sorted(p for b in buf for p in b)
+    else:
+        covered = prompts
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": args.scaling, "max_over_ranks": tmax,
+                          "prompts_per_rank": counts, "prompts_covered": len(set(covered)),
+                          "global_tokens": len(covered) if args.scaling == "strong" else N_PROMPTS * world}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -683,6 +714,8 @@ def main():
     ap.add_argument("--layers", type=int, default=N_LAYERS, help=argparse.SUPPRESS)
     ap.add_argument("--secondary", type=int, default=1, help="also run configs 1-3 (secondary objects)")
     ap.add_argument("--cpu", type=int, default=1, help="time the reference CPU path (rank 0, N=1)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (no GPU): ranks, gloo process group, prompt partition, max-over-ranks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -695,6 +728,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
 
+    if args.dry_run:
+        dry_run(args, rank, world)
+        return
     if args.impl == "reference":
         if rank != 0:
             return

@@ -120,3 +120,25 @@ def test_partition_helpers_single_process():
     with pytest.raises(ValueError):
         sh.local_ids([2])
     assert pgd.max_over_ranks(3.0) == 3.0
+
+
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_gpus_2_spawns_ranks(scaling):
+    """`bench.py --gpus 2` re-executes itself under torch.distributed.run (one
+    process per GPU); the dry run exercises that launch path on CPU: 2 ranks in
+    a gloo group, the prompt partition (strong: 256 global prompts split by
+    pattern affinity, weak: 256 per rank) and the max-over-ranks reduction."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, MASTER_PORT="29631")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run", "--scaling",
+                        scaling], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["max_over_ranks"] == 2.0
+    if scaling == "strong":
+        assert line["prompts_per_rank"] == [128, 128] and line["prompts_covered"] == 256
+    else:
+        assert line["prompts_per_rank"] == [256, 256] and line["global_tokens"] == 512

@@ -44,3 +44,52 @@ def test_peer_reduce_fused_allreduce(pg, port, world, m, n, r, K):
         ref = port.masked_forward(bfr(A), bfr(B), sel, x.double().cpu().numpy()[:, None])[:, 0]
         y = outs[0].double().cpu().numpy()
         assert np.abs(y - ref).max() / np.abs(ref).max() <= 1e-4
+
+
+def _ipc_worker(rank, world, init, q):
+    import ctypes as C
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=init, rank=rank, world_size=world)
+    from paper_2605_08568_b200.dist import PeerReduceLinear
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((256, 96)) / 16.0
+    B = rng.standard_normal((128, 96)) / 11.0
+    pr = PeerReduceLinear(A, B, world, rank, dtype="bf16", group=dist.group.WORLD)
+    assert pr.peer_ptrs[rank] == pr.recv.data_ptr() and len(pr._opened) == world - 1
+    # every rank writes its id into its right neighbour's receive buffer through
+    # the IPC-opened pointer, then reads its own buffer
+    cudart = C.CDLL("/usr/local/cuda/lib64/libcudart.so")
+    src = torch.full((16,), 1000 + rank, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    dst = (rank + 1) % world
+    rc = cudart.cudaMemcpy(C.c_void_p(pr.peer_ptrs[dst]), C.c_void_p(src.data_ptr()), C.c_size_t(16 * 8), 3)
+    torch.cuda.synchronize()
+    dist.barrier()
+    got = pr.recv[:16].cpu().tolist()
+    pr.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, rc, got))
+
+
+def test_peer_ipc_exchange_two_processes(tmp_path):
+    """PeerReduceLinear._exchange across real processes: receive-buffer IPC
+    handles all-gathered over a gloo group, opened with pg_ipc_open_handle, and
+    written through by the neighbour rank (two processes on the one reachable
+    GPU; the fused kernel itself runs in the virtual-rank test above)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = 2
+    init = f"file://{tmp_path}/rdzv"
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, init, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, rc, got in res:
+        assert rc == 0
+        assert got == [1000 + (rank - 1) % world] * 16
