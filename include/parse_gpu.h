@@ -218,6 +218,14 @@ int pg_module_forward(const pg_agg* layers, size_t n_linears, const size_t* patt
 int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns_host,
                    const int32_t* pattern_dev, const void* x_dev, void* act_dev, void* y_dev,
                    pg_dtype y_dtype, pg_stream stream);
+/* A chain of S MLP blocks as in pg_mlp_forward, block s+1 reading block s's
+ * output (x_{s+1} = y_s; y in the weight dtype when S > 1): patterns [S][3]
+ * (up, gate, down), acts[s] optional (null array or entries: workspace),
+ * ys[s] the blocks' outputs.  Up to 8 blocks per launch: the weight stream
+ * runs through each block's last exchange and the launch boundary. */
+int pg_mlp_forward_chain(const pg_agg* ups, const pg_agg* gates, const pg_agg* downs, const size_t* patterns,
+                         size_t S, const void* x_dev, void* const* acts_dev, void* const* ys_dev, pg_dtype y_dtype,
+                         pg_stream stream);
 
 /* Union-masked heterogeneous batch (BASELINE config 4: decode batch of
  * prompts, each with its own selection): masked_forward (rank_experts.hpp:52-72)

@@ -103,6 +103,7 @@ _SIGS = {
     "pg_pack_selected": [_vp, _vp, _sz, _sz, _vp, _vp, _vp],
     "pg_prefill_packed": [_vp, _vp, _vp, _sz, _i64p, _sz, _vp, _vp, _i, _vp],
     "pg_mlp_forward": [_vp, _vp, _vp, _sp, _vp, _vp, _vp, _vp, _i, _vp],
+    "pg_mlp_forward_chain": [_vp, _vp, _vp, _sp, _sz, _vp, _vp, _vp, _i, _vp],
 }
 _VOID = {
     "pg_rng_fill_gaussian": [C.c_uint64, _dp, _sz],

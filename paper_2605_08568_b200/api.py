@@ -1070,6 +1070,29 @@ def mlp_forward(up: "AggregatedLayer", gate: "AggregatedLayer", down: "Aggregate
     return y
 
 
+def mlp_forward_chain(blocks, x: torch.Tensor, pattern_ids=None, outs=None, acts=None) -> list:
+    """A decode token through a chain of MLP blocks, block s+1 reading block
+    s's output (x_{s+1} = y_s, every block as mlp_forward), up to 8 blocks per
+    kernel launch (pg_mlp_forward_chain).  blocks: [(up, gate, down), ...]
+    aggregated layers; pattern_ids: per block (up, gate, down) pattern ids
+    (default 0).  Returns the blocks' outputs (weight dtype)."""
+    S = len(blocks)
+    if S < 1:
+        raise ValueError("mlp_forward_chain: no blocks")
+    dt = blocks[0][0].layer.torch_dtype
+    x = _dev(x, dt).reshape(-1)
+    ys = outs if outs is not None else [torch.empty(b[2].m, dtype=dt, device="cuda") for b in blocks]
+    if len(ys) != S or any(y.dtype != dt or not y.is_contiguous() or y.numel() != b[2].m for y, b in zip(ys, blocks)):
+        raise ValueError("mlp_forward_chain: one contiguous output of the weight dtype per block")
+    pids = pattern_ids if pattern_ids is not None else [(0, 0, 0)] * S
+    pat = (C.c_size_t * (3 * S))(*[int(v) for p in pids for v in p])
+    hs = [(C.c_void_p * S)(*[b[i].handle.value for b in blocks]) for i in range(3)]
+    ap = (C.c_void_p * S)(*[_ptr(a) for a in acts]) if acts is not None else None
+    yp = (C.c_void_p * S)(*[_ptr(y) for y in ys])
+    call("pg_mlp_forward_chain", hs[0], hs[1], hs[2], pat, S, _ptr(x), ap, yp, _dtype_code(dt), _stream())
+    return ys
+
+
 def copy_io(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
     """Step I/O as a kernel on the current stream: dst <- src where either side
     may be pinned host memory (UVA-mapped).  Chains with the step's kernels

@@ -585,6 +585,8 @@ static char* chain_workspace(cudaStream_t st, size_t bytes, int grid, const void
     return w.first;
 }
 
+static size_t chain_tab_bytes(size_t nphase) { return std::max<size_t>(1024, round_up(nphase * kMaxLin * kLinSBytes, 128)); }
+
 // Chain feasibility: contiguous runs only (no gather list) and the largest
 // streamed item (a B^T row, or an up/gate A-row pair) fits one ring stage.
 static size_t chain_chunk_bytes(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, bool mlp,
@@ -602,12 +604,12 @@ static size_t chain_chunk_bytes(pg_dtype wdt, const std::vector<std::vector<LinS
             item = std::max(item, (size_t)l.cap * es);
             pair += (size_t)l.cap * es;
         }
-        if (mlp && p == 0) item = std::max(item, pair);
+        if (mlp && p % 2 == 0) item = std::max(item, pair);  // up/gate A-row pairs
         zs = std::max(zs, round_up(zsum, 128));
     }
     *xs_bytes = xs;
     *zs_bytes = zs;
-    const size_t fixed = 1024 + xs + zs + kRingStages * (128 + 16) + 128;
+    const size_t fixed = chain_tab_bytes(phases.size()) + xs + zs + kRingStages * (128 + 16) + 128;
     const size_t kMaxSmem = 227 * 1024;
     if (fixed + 2 * item > kMaxSmem) return 0;  // need >= 2 stages in flight
     static const int div_env = [] {  // experiments: size chunks for this many stages
@@ -631,11 +633,38 @@ struct PeerSpec {  // expert-sharded peer reduction (ChainParams::npeer)
     void* const* bufs = nullptr;
 };
 
+// Per-phase inputs of a chain: x (the phase input), act (MLP epilogue target,
+// also the next phase's input), epilogue kind.  A chain of S MLP blocks has
+// 2S phases: {up_s, gate_s} (epilogue 1 into act_s) and {down_s} (x = act_s,
+// y_s); block s+1 reads y_s.
+struct ChainIO {
+    std::vector<const void*> x;
+    std::vector<void*> act;
+    std::vector<int> epi;
+};
+
+static void run_chain_io(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, ChainIO io, bool mlp,
+                         pg_dtype ydt, cudaStream_t st, const PeerSpec* peer);
+
 static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, const void* x,
                       bool mlp, void* act, pg_dtype ydt, cudaStream_t st, const PeerSpec* peer = nullptr) {
+    ChainIO io;
+    for (size_t p = 0; p < phases.size(); ++p) {
+        io.x.push_back(p == 0 ? x : nullptr);  // null: the workspace act (MLP phase 1)
+        io.act.push_back(act);
+        io.epi.push_back((mlp && p == 0) ? 1 : 0);
+    }
+    run_chain_io(wdt, phases, io, mlp, ydt, st, peer);
+}
+
+static void run_chain_io(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& phases, ChainIO io, bool mlp,
+                         pg_dtype ydt, cudaStream_t st, const PeerSpec* peer) {
     const size_t accs = wdt == PG_F64 ? 8 : 4, es = dtype_size(wdt);
+    if (phases.empty() || phases.size() > (size_t)kMaxPhase)
+        throw Error{PG_INVALID_ARGUMENT, "decode chain: 1..16 phases"};
     ChainParams P = {};
     P.nphase = (int)phases.size();
+    P.tab_bytes = (int)chain_tab_bytes(phases.size());
     size_t xs_bytes = 0, zs_bytes = 0;
     const size_t ch = chain_chunk_bytes(wdt, phases, mlp, &xs_bytes, &zs_bytes);
     if (!ch) throw Error{PG_INVALID_ARGUMENT, "decode chain: operands exceed shared memory"};
@@ -670,7 +699,15 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
     size_t zbytes = 256;
     for (auto& ph : phases)
         for (auto& l : ph) zbytes += round_up((size_t)l.cap * zw * 8, 256);
-    const size_t act_bytes = (mlp && !act) ? round_up((size_t)phases[0][0].m * es, 256) : 0;
+    // workspace act for MLP blocks given none (one per block: a block's act is
+    // read by its down phase while the next block may already write its own)
+    size_t act_bytes = 0;
+    std::vector<size_t> act_off(phases.size(), (size_t)-1);
+    for (size_t p = 0; p < phases.size(); ++p)
+        if (io.epi[p] == 1 && !io.act[p]) {
+            act_off[p] = act_bytes;
+            act_bytes += round_up((size_t)phases[p][0].m * es, 256);
+        }
     // Persistent per-stream workspace: [barrier counter | epoch | z words | act].
     // The barrier counter is monotone (every launch adds a multiple of the grid
     // size) and z words carry their launch's tag, so consecutive chain launches
@@ -698,14 +735,17 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
     }();
     P.ztag = ztag_env >= 0 ? ztag_env : (mlp ? 1 : 0);
     size_t off = 256;
-    if (act_bytes) act = base + zbytes;
+    for (size_t p = 0; p < phases.size(); ++p)
+        if (act_off[p] != (size_t)-1) io.act[p] = base + zbytes + act_off[p];
     for (size_t p = 0; p < phases.size(); ++p) {
         ChainPhase& Q = P.ph[p];
         Q.nlin = (int)phases[p].size();
-        Q.x = p == 0 ? x : act;
-        Q.epilogue = (mlp && p == 0) ? 1 : 0;
+        // a phase without an explicit x reads the previous phase's act
+        Q.x = io.x[p] ? io.x[p] : (p > 0 ? io.act[p - 1] : nullptr);
+        if (!Q.x) throw Error{PG_INVALID_ARGUMENT, "decode chain: phase without input"};
+        Q.epilogue = io.epi[p];
         Q.ydt = ydt;
-        Q.act = act;
+        Q.act = io.act[p];
         for (int l = 0; l < Q.nlin; ++l) {
             const LinSpec& S = phases[p][l];
             ChainLin& L = Q.lin[l];
@@ -720,7 +760,8 @@ static void run_chain(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& pha
         P.prank = peer->rank;
         for (int r = 0; r < peer->npeer; ++r) P.peer_recv[r] = static_cast<unsigned long long*>(peer->bufs[r]);
     }
-    const size_t total = 1024 + xs_bytes + zs_bytes + kRingStages * (128 + 16) + 128 + (size_t)kRingStages * ch;
+    const size_t total = chain_tab_bytes(phases.size()) + xs_bytes + zs_bytes + kRingStages * (128 + 16) + 128 +
+                         (size_t)kRingStages * ch;
     launch_chain(wdt, P, std::min(total, (size_t)227 * 1024), st, grid);
 }
 
@@ -1387,6 +1428,47 @@ int pg_mlp_forward(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, 
         launch_silu_mul(g, u, mid, (size_t)up->m, a, up->dt, st);
         const LinSpec& D = ph[1][0];
         run_forward(up->dt, D.bt, D.ldb, D.a, D.lda, D.sm, D.cap, D.n, D.m, a, 0, 1, y, ydt, st);
+    }
+    PG_API_END
+}
+
+// A chain of S MLP blocks (x_{s+1} = y_s) through the decode chain, up to 8
+// blocks per launch: the weight producer streams block s+1's rows through
+// block s's last exchanges and the launch boundary disappears.
+int pg_mlp_forward_chain(const pg_agg* ups, const pg_agg* gates, const pg_agg* downs, const size_t* patterns,
+                         size_t S, const void* x, void* const* acts, void* const* ys, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(ups && gates && downs && patterns && x && ys && S >= 1, PG_INVALID_ARGUMENT,
+            "mlp_forward_chain: bad arguments");
+    const pg_dtype wdt = ups[0]->dt;
+    for (size_t b = 0; b < S; ++b) {
+        const pg_agg up = ups[b], gate = gates[b], down = downs[b];
+        require(up && gate && down && ys[b], PG_INVALID_ARGUMENT, "mlp_forward_chain: bad arguments");
+        require(up->dt == wdt && gate->dt == wdt && down->dt == wdt, PG_INVALID_ARGUMENT, "mlp_forward_chain: mixed dtypes");
+        require(up->m == gate->m && up->n == gate->n && down->n == up->m && down->m == up->n, PG_INVALID_ARGUMENT,
+                "mlp_forward_chain: shape mismatch (up/gate m x n, down n x m, blocks chained)");
+    }
+    check_ydt(wdt, ydt);
+    require(S == 1 || ydt == wdt, PG_INVALID_ARGUMENT, "mlp_forward_chain: chained blocks need y in the weight dtype");
+    const cudaStream_t st = as_stream(s);
+    for (size_t b0 = 0; b0 < S; b0 += kMaxPhase / 2) {
+        const size_t nb = std::min<size_t>(kMaxPhase / 2, S - b0);
+        std::vector<std::vector<LinSpec>> ph;
+        ChainIO io;
+        for (size_t b = b0; b < b0 + nb; ++b) {
+            const size_t* pt = patterns + 3 * b;
+            ph.push_back({agg_spec(ups[b], (int)pt[0], nullptr, nullptr), agg_spec(gates[b], (int)pt[1], nullptr, nullptr)});
+            ph.push_back({agg_spec(downs[b], (int)pt[2], nullptr, ys[b])});
+            io.x.push_back(b == 0 ? x : ys[b - 1]);
+            io.x.push_back(nullptr);
+            void* a = acts ? acts[b] : nullptr;
+            io.act.push_back(a);
+            io.act.push_back(a);
+            io.epi.push_back(1);
+            io.epi.push_back(0);
+        }
+        require(chain_ok(wdt, ph, true), PG_INVALID_ARGUMENT, "mlp_forward_chain: block too wide for the decode chain");
+        run_chain_io(wdt, ph, io, true, ydt, st, nullptr);
     }
     PG_API_END
 }

@@ -9,7 +9,8 @@ constexpr int kChainThreads = 384;
 constexpr int kChainWarps = kChainThreads / 32;
 constexpr int kConsumerWarps = kChainWarps - 1;  // warp 15 is the TMA producer
 constexpr int kMaxLin = 3;
-constexpr int kMaxPhase = 2;
+constexpr int kMaxPhase = 16;  // 2 per MLP block: up to 8 chained blocks per launch
+constexpr int kLinSBytes = 128;  // shared-memory table entry per (phase, linear)
 constexpr int kRingStages = 8;
 constexpr int kMaxChunkItems = 16;
 constexpr int kMaxPeers = 8;
@@ -29,7 +30,7 @@ struct ChainLin {
 struct ChainPhase {
     int nlin;
     ChainLin lin[kMaxLin];
-    const void* x;  // [n] phase input (storage dtype); phase 1 reads the phase-0 act
+    const void* x;  // [n] phase input (storage dtype): the block input, the block's act, or the previous block's y
     int epilogue;   // 0: y_l per linear (ydt); 1: act = silu(y_1) * y_0 -> act (storage dtype)
     int ydt;
     void* act;
@@ -37,6 +38,7 @@ struct ChainPhase {
 
 struct ChainParams {
     int nphase;
+    int tab_bytes;  // shared-memory tables: nphase * kMaxLin * kLinSBytes (>= 1024)
     ChainPhase ph[kMaxPhase];
     unsigned long long* bar;    // grid-barrier counter (act hand-over between MLP phases)
     unsigned long long* epoch;  // launch counter (each CTA adds 1 per launch): z-word tags

@@ -60,6 +60,7 @@ struct LinS {
     int i0, i1;  // this CTA's stage-2 row range
     int pad[2];
 };
+static_assert(sizeof(LinS) <= kLinSBytes, "LinS table entry");
 struct Desc {
     int seg, lin, count, gidx, last;
     int ids[kMaxChunkItems];
@@ -175,7 +176,7 @@ __device__ __forceinline__ void stage_batched(T* dst, const T* __restrict__ src,
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int e = base + u * nthr + tid;
-            if (e < count) v[u] = src[e];
+            if (e < count) v[u] = __ldcg(src + e);  // L2: x may be another CTA's output of this launch
         }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
@@ -457,11 +458,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
 
-    // ---- carve shared memory: [tables 1K][x][z][descs][full][empty][ring]
+    // ---- carve shared memory: [tables][x][z][descs][full][empty][ring]
     LinS* lins = reinterpret_cast<LinS*>(smem);
-    W* xs = reinterpret_cast<W*>(smem + 1024);
-    A* zs = reinterpret_cast<A*>(smem + 1024 + P.xs_bytes);
-    Desc* descs = reinterpret_cast<Desc*>(smem + 1024 + P.xs_bytes + P.zs_bytes);
+    const int tb = P.tab_bytes;
+    W* xs = reinterpret_cast<W*>(smem + tb);
+    A* zs = reinterpret_cast<A*>(smem + tb + P.xs_bytes);
+    Desc* descs = reinterpret_cast<Desc*>(smem + tb + P.xs_bytes + P.zs_bytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(descs + kRingStages);
     uint64_t* empty = full + kRingStages;
     const size_t ring_off = ((size_t)(reinterpret_cast<unsigned char*>(empty + kRingStages) - smem) + 16 + 127) & ~size_t(127);
@@ -469,13 +471,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
     const int nst = (int)min((size_t)min(P.max_stages, kRingStages), (size_t)(227 * 1024 - ring_off) / (size_t)P.chunk_bytes);
 
     STAMP(0);
-    if (threadIdx.x < P.nphase * kMaxLin) {
-        const int ph = threadIdx.x / kMaxLin, l = threadIdx.x % kMaxLin;
+    for (int t = threadIdx.x; t < P.nphase * kMaxLin; t += blockDim.x) {
+        const int ph = t / kMaxLin, l = t % kMaxLin;
         const ChainPhase& Q = P.ph[ph];
         if (l < Q.nlin) {
             const ChainLin& C = Q.lin[l];
             const SlotMap sm = resolve(C.sm);
-            LinS& L = lins[threadIdx.x];
+            LinS& L = lins[t];
             L.bt = static_cast<const char*>(C.bt);
             L.a = static_cast<const char*>(C.a);
             L.mask = sm.mask;
@@ -541,14 +543,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             const int nbytes = n * es;
             stage_batched<int4, 4>(reinterpret_cast<int4*>(xs), reinterpret_cast<const int4*>(Q.x), nbytes / 16,
                                    tid, nct);
-            for (int e = (nbytes / 16) * 16 / es + tid; e < n; e += nct) xs[e] = static_cast<const W*>(Q.x)[e];
+            for (int e = (nbytes / 16) * 16 / es + tid; e < n; e += nct) xs[e] = __ldcg(static_cast<const W*>(Q.x) + e);
             for (int e = n + tid; e < (n + V - 1) / V * V; e += nct) xs[e] = W(0);
         }
         if (ph == 0) STAMP(6);  // x staged (thread 0), before the launch tag is needed
         if (ph == 0 && threadIdx.x == 0) *tag_s = (uint32_t)(epoch_old / (unsigned long long)G) + 1u;
         consumer_sync();
         const uint32_t tag = *tag_s;
-        STAMP(ph * 6 + 1);
+        if (ph < 2) STAMP(ph * 6 + 1);
         // ---- stage 1: z_s = B^T[s] . x
         for (;;) {
             mbar_wait(smem_u32(&full[k]), (par >> k) & 1u);
@@ -592,9 +594,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             k = (k + 1 == nst) ? 0 : k + 1;
             if (last) break;
         }
-        STAMP(ph * 6 + 2);
+        if (ph < 2) STAMP(ph * 6 + 2);
         if (!P.ztag) grid_sync_consumers(P.bar);
-        STAMP(ph * 6 + 3);
+        if (ph < 2) STAMP(ph * 6 + 3);
         // ---- z into shared memory (inactive slots -> 0)
         int zoff[kMaxLin];
         {
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             }
         }
         consumer_sync();
-        STAMP(ph * 6 + 4);
+        if (ph < 2) STAMP(ph * 6 + 4);
         if (P.throttle >= 0 && threadIdx.x == 0) mbar_arrive(smem_u32(empty + kRingStages + 1));
         // bf16 with <= 2 linears of <= 32 * 8 * kRowJ slots: z into registers
         ZReg zr0, zr1;
@@ -744,7 +746,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             k = (k + 1 == nst) ? 0 : k + 1;
             if (last) break;
         }
-        STAMP(ph * 6 + 5);
+        if (ph < 2) STAMP(ph * 6 + 5);
         if (ph + 1 < P.nphase) grid_sync_consumers(P.bar);  // act complete before phase ph+1 reads it
     }
     if constexpr (PEER) {

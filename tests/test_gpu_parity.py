@@ -663,3 +663,41 @@ def test_config5_13b_shapes_decode_and_prefill(pg, port):
     y = pg.masked_forward(L, pg.RankSelection(sel), torch.from_numpy(x).cuda().to(torch.bfloat16))
     # prefill rounds z to bf16 between the two tcgen05 stages
     assert rel(y.double().cpu().numpy(), port.masked_forward(Ar, Br, sel, bf16_round(x))) <= 1e-2
+
+
+@pytest.mark.parametrize("nblocks,d,ff", [(3, 512, 1376), (10, 4096, 11008)])
+def test_mlp_forward_chain_matches_blockwise(pg, port, nblocks, d, ff):
+    """A decode token through a chain of MLP blocks (x_{s+1} = y_s) in <= 8
+    blocks per launch (pg_mlp_forward_chain) is bit-identical to one
+    mlp_forward launch per block (same CTA ranges and reduction orders), and
+    the first block matches the oracle composition.  10 blocks: two launches."""
+    K = pg.single_layer_k(ff, d, 0.6); r = pg.store_rank(K, d)
+    from oracle import pyoracle
+    pats = pyoracle.make_patterns(17171, 2, [(r, K)] * 3)
+    blocks, raw = [], []
+    for b in range(min(nblocks, 4)):  # 4 weight replicas, rotated
+        data = {nm: make_layer_data(port, *(shp + (r, 200 + 10 * b + i))) for i, (nm, shp) in
+                enumerate([("up", (ff, d)), ("gate", (ff, d)), ("down", (d, ff))])}
+        aggs = tuple(pg.aggregate_layout(pg.FactorizedLayer(*data[nm], K, dtype="bf16"),
+                                         [pg.RankSelection(p[i]) for p in pats], 0.9)
+                     for i, nm in enumerate(("up", "gate", "down")))
+        blocks.append(aggs)
+        raw.append(data)
+    chain = [blocks[s % len(blocks)] for s in range(nblocks)]
+    pids = [(s % 2, (s + 1) % 2, s % 2) for s in range(nblocks)]
+    x = torch.from_numpy(port.gaussian(210, (d,))).cuda().to(torch.bfloat16)
+    ys = pg.mlp_forward_chain(chain, x, pids)
+    h = x
+    for s, (up, gate, down) in enumerate(chain):
+        y = pg.mlp_forward(up, gate, down, pids[s], h,
+                           out_dtype=torch.bfloat16)
+        assert torch.equal(ys[s], y), s
+        h = y
+    assert torch.isfinite(ys[-1].float()).all()
+    # block 0 vs the oracle (f64 on the bf16-rounded operands)
+    rd = {nm: (bf16_round(A), bf16_round(B)) for nm, (A, B) in raw[0].items()}
+    xr = x.double().cpu().numpy()[:, None]
+    u = port.masked_forward(*rd["up"], pats[pids[0][0]][0], xr)
+    g = port.masked_forward(*rd["gate"], pats[pids[0][1]][1], xr)
+    ref = port.masked_forward(*rd["down"], pats[pids[0][2]][2], bf16_round(_silu(g) * u))
+    assert rel(ys[0].double().cpu().numpy()[:, None], ref) <= 4e-3
