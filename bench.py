@@ -671,6 +671,103 @@ def config1_arm(args, local_rank, cpu: bool):
     return out
 
 
+# ======================================================================= config 5 (13B, expert-sharded)
+
+LIN13 = {"q": (5120, 5120), "k": (5120, 5120), "v": (5120, 5120), "o": (5120, 5120),
+         "up": (13824, 5120), "gate": (13824, 5120), "down": (5120, 13824)}
+
+
+def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
+    """BASELINE config 5: one LLaMA-13B-shaped decoder layer's 7 rank-expert
+    linears at ratio 0.4 (K = 1536 / 2241, r_store = 3072 / 4482: stored experts
+    exceed dense storage), expert-sharded (expert e on rank e mod G,
+    dist.py), mixed work per step: a T=256 prefill chunk then 8 decode tokens,
+    every linear's partial all-reduced over NCCL (the only collective).  Each
+    rank holds 1/G of the experts (weights generated on device for the rank's
+    own columns); selections from the reference generator."""
+    import torch
+    import paper_2605_08568_b200 as pg
+    from paper_2605_08568_b200 import dist as pgd
+    dev = torch.device("cuda", local_rank)
+    g = torch.Generator(device=dev).manual_seed(13 + rank)
+    ldims = {}
+    for nm, (m, n) in LIN13.items():
+        K = pg.single_layer_k(m, n, 0.4)
+        ldims[nm] = (pg.store_rank(K, n), K)
+    pats = pg.make_patterns(5151, 1, [ldims[nm] for nm in LIN13])[0]
+    lins = {}
+    for j, (nm, (m, n)) in enumerate(LIN13.items()):
+        r, K = ldims[nm]
+        cols = len(range(rank, r, world))
+        bt = (torch.randn(cols, n, device=dev, generator=g) / n ** 0.5).to(torch.bfloat16)
+        a = (torch.randn(m, cols, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
+        mine = pgd.shard_selection(pats[j], world, rank)
+        loc = (mine // world).astype(np.uint32) if mine.size else np.zeros(1, np.uint32)
+        L = pg.FactorizedLayer.from_device(bt, a, int(loc.size), layer_id=f"b0.{nm}")
+        agg = pg.aggregate_layout(L, [pg.RankSelection(loc)], 0.9)
+        lins[nm] = (agg, m, n, mine.size)
+    xp = torch.randn(T_pre, 5120, device=dev, generator=g).to(torch.bfloat16)
+    xd = torch.randn(5120, device=dev, generator=g).to(torch.bfloat16)
+    xpf = torch.randn(T_pre, 13824, device=dev, generator=g).to(torch.bfloat16)
+    xdf = torch.randn(13824, device=dev, generator=g).to(torch.bfloat16)
+    yp = {nm: torch.empty(T_pre, m, device=dev) for nm, (_, m, _, _) in lins.items()}
+    yd = {nm: torch.empty(m, device=dev) for nm, (_, m, _, _) in lins.items()}
+    st = torch.cuda.Stream(device=dev)
+
+    def reduce(y):
+        if world > 1:
+            torch.distributed.all_reduce(y)
+
+    def step():
+        for nm, (agg, m, n, own) in lins.items():  # prefill chunk: T=256 tokens through each linear
+            x = xpf if n == 13824 else xp
+            pg.aggregated_forward_batched(agg, [0], [0, T_pre], x, out_dtype=torch.float32, out=yp[nm])
+            reduce(yp[nm])
+        for _ in range(n_dec):  # decode tokens reusing S
+            for nm, (agg, m, n, own) in lins.items():
+                pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
+                reduce(yd[nm])
+
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            step()
+    st.synchronize()
+    barrier(torch, world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(reps):
+            step()
+        e1.record(st)
+    st.synchronize()
+    ms = max_over_ranks(torch, e0.elapsed_time(e1) / reps, dev, world)
+    # decode alone (the HBM-bound part): 8 tokens through the 7 sharded linears
+    with torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(reps):
+            for nm, (agg, m, n, own) in lins.items():
+                pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
+                reduce(yd[nm])
+        e1.record(st)
+    st.synchronize()
+    us_dec = max_over_ranks(torch, e0.elapsed_time(e1) / reps * 1e3, dev, world)
+    hbm_peak, tensor_peak, peak_kind = peaks()
+    dec_bytes = sum(own * (m + n) * 2 for (_, m, n, own) in lins.values())  # this rank's selected experts
+    flops = 2 * T_pre * sum(ldims[nm][1] * (m + n) for nm, (m, n) in LIN13.items())
+    return {"workload": f"config5: LLaMA-13B decoder layer (q,k,v,o 5120x5120, gate/up 5120->13824, down "
+                        f"13824->5120) ratio 0.4, expert-sharded over {world} GPU(s) (e mod G), per step 1 x "
+                        f"T={T_pre} prefill chunk + {n_dec} decode tokens through all 7 linears, partial outputs "
+                        f"all-reduced (NCCL) per linear; bf16 weights, f32 outputs",
+            "ms_per_step": ms, "tokens_per_s": (T_pre + n_dec) / (ms * 1e-3),
+            "decode_us_per_token": us_dec, "decode_tokens_per_s": 1e6 / us_dec,
+            "decode_roofline": {"bound": "hbm", "alg_bytes_per_token_rank0": dec_bytes,
+                                "achieved": dec_bytes / (us_dec * 1e-6) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                "frac": dec_bytes / (us_dec * 1e-6) / 1e9 / hbm_peak, "peak_kind": peak_kind},
+            "prefill_flops_per_step": flops,
+            "collective": "torch.distributed.all_reduce (NCCL) of every linear's partial" if world > 1
+            else "none (world 1: one shard holds every expert)"}
+
+
 # ======================================================================= main
 
 def dry_run(args, rank, world):
@@ -758,6 +855,7 @@ def main():
     if args.secondary:
         out["decode_b1"] = config2_arm(args, rank, world, local_rank)
         out["prefill"] = config3_arm(args, rank, world, local_rank)
+        out["config5"] = config5_arm(args, rank, world, local_rank)
         if rank == 0:
             out["config1"] = config1_arm(args, local_rank, cpu=bool(args.cpu) and world == 1)
     if rank == 0 and world == 1 and args.cpu:
