@@ -57,7 +57,7 @@ namespace pg {
 constexpr int UP_STAGES = UP_STAGES_CFG;
 constexpr int UP_STAGE_BYTES = WM_W_BYTES + WM_X_BYTES;  // 32 KB
 #ifndef UP_EPI_WARPS_CFG
-#define UP_EPI_WARPS_CFG 8
+#define UP_EPI_WARPS_CFG 4
 #endif
 constexpr int UP_EPI_WARPS = UP_EPI_WARPS_CFG;  // 4 or 8: 1 or 2 warps per TMEM lane quadrant
 constexpr int UP_EPI_T = 32 * UP_EPI_WARPS;

@@ -1,0 +1,5 @@
+timeout 300 python -m pytest tests/test_gpu_union_prog.py -x -q 2>&1 | grep -E "passed|failed|^E  .*assert|^FAILED" | head -6
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+PG_PROG_DBG=1 timeout 200 python tools/experiments/exp_prog.py 2 2>&1 | tail -9
+timeout 200 python tools/experiments/exp_prog.py 32 2>&1 | grep "program:"
+PG_PROG_KEEP=0 timeout 200 python tools/experiments/exp_prog.py 32 2>&1 | grep "program:"
