@@ -284,6 +284,41 @@ std::size_t ref_single_layer_k(std::size_t m, std::size_t n, double ratio) {
     return allocate_budgets({spectrum}, {{m, n}}, ratio)[0];
 }
 
+// router.hpp:318-400 train_router_matrix on caller data: nseq sequences,
+// sequence s has T[s] tokens, x_s (n x T_s) and y_s (m x T_s) concatenated
+// row-major; outputs the returned (best-epoch) router and both loss curves.
+int ref_train_router(const double* A, const double* B, std::size_t m, std::size_t n, std::size_t r, std::size_t K,
+                     std::size_t nseq, const std::size_t* T, const double* xs, const double* ys, double lr,
+                     std::size_t epochs, std::size_t batch, double warmup, double wd, std::uint64_t seed,
+                     double tau, double* theta_out, double* bias_out, double* epoch_loss, double* frozen_loss) {
+    try {
+        FactorizedLayer fl = make_layer(A, B, m, n, r);
+        fl.K = K;
+        std::vector<RouterSeqStats> seqs;
+        std::size_t ox = 0, oy = 0;
+        for (std::size_t s = 0; s < nseq; ++s) {
+            seqs.push_back(precompute_router_stats(fl, to_mat(xs + ox, n, T[s]), to_mat(ys + oy, m, T[s])));
+            ox += n * T[s];
+            oy += m * T[s];
+        }
+        RouterTrainConfig cfg;
+        cfg.learning_rate = lr;
+        cfg.epochs = epochs;
+        cfg.batch_size = batch;
+        cfg.warmup_frac = warmup;
+        cfg.weight_decay = wd;
+        cfg.seed = seed;
+        RouterTrainResult res = train_router_matrix(fl, seqs, cfg, tau);
+        std::memcpy(theta_out, res.params.theta.data(), r * n * sizeof(double));
+        std::memcpy(bias_out, res.params.bias.data(), r * sizeof(double));
+        std::memcpy(epoch_loss, res.epoch_loss.data(), epochs * sizeof(double));
+        std::memcpy(frozen_loss, res.frozen_loss.data(), epochs * sizeof(double));
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
 void ref_fill_gaussian(std::uint64_t seed, double* out, std::size_t count) {
     Rng rng(seed);
     for (std::size_t i = 0; i < count; ++i) out[i] = rng.gaussian();

@@ -60,6 +60,7 @@ struct __align__(64) UmmaParams {
     UmmaGroup groups[UM_MAX_GROUPS];
     int ngroups;
     int total_tiles;
+    int epi_deep;  // bf16 TMA-store epilogue: 4 x 2 KB staging slots per warp in flight (else 2)
 };
 
 // ---- epilogue helpers: TMEM -> registers -> bf16 / f32 -> global, with the
@@ -297,10 +298,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
                  : "memory");
 }
 __device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUtensorMap* omap, uint32_t tbase, int q,
-                                                  int lane, int row0, int n0, unsigned char* stage, int& nbuf) {
+                                                  int lane, int row0, int n0, unsigned char* stage, int& nbuf,
+                                                  int epi_deep) {
     const int nch = (G.bn + 31) / 32;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const int es = G.out_bf16 ? 2 : 4;
+    // the warp's 8 KB of staging: 2 slots of a 32 x 32 f32 box, or (bf16) 4
+    // slots of 2 KB -- stores in flight per warp bound the drain of short-K tiles
+    const bool deep = epi_deep && G.out_bf16;
+    const int slot_bytes = 32 * 32 * es;
     uint32_t ra[32], rb[32];
     auto emit = [&](int c, uint32_t (&r)[32]) {
         const int c0 = 32 * c;
@@ -309,8 +315,11 @@ __device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUte
             store_chunk(G, row0 + lane, n0, c0, r);
             return;
         }
-        unsigned char* buf = stage + (nbuf & 1) * U2_OUT_BYTES;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buf's previous store read it
+        unsigned char* buf = stage + (deep ? (nbuf & 3) * slot_bytes : (nbuf & 1) * U2_OUT_BYTES);
+        if (lane == 0) {  // buf's previous store has read it
+            if (deep) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         __syncwarp();
         unsigned char* dst = buf + lane * 32 * es;
         if (G.out_bf16) {
@@ -466,7 +475,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
             if (G.direct_epi) epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
-            else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf);
+            else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf,
+                                   P.epi_deep);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
@@ -598,7 +608,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped4(const __grid_co
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
             if (G.direct_epi) epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
-            else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf);
+            else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf,
+                                   P.epi_deep);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
@@ -766,6 +777,11 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
         }
         P->ngroups = ng;
         P->total_tiles = tiles;
+        static const int epi_env = [] {
+            const char* e = getenv("PG_UMMA_EPI_DEEP");
+            return e ? atoi(e) : 1;
+        }();
+        P->epi_deep = epi_env;
         if (tiles == 0) continue;
         if (mc) {
             static int max_cl = [&] {
