@@ -60,6 +60,71 @@ k_cosine_scan(const double* __restrict__ emb, const double* __restrict__ q, int 
     }
 }
 
+// Wide scan (d a multiple of 8): WPE warps per entry, EPB entries per block,
+// each lane keeping 8 double2 loads in flight (the one-warp-per-entry scan
+// leaves ~4 KB in flight per warp: latency-bound at N = 1024).  Partial sums
+// meet in shared memory; the bound argument is order-independent.
+constexpr int kCosWPE = 4, kCosEPB = 2;
+__global__ void __launch_bounds__(kCosWPE * kCosEPB * 32)
+k_cosine_scan_wide(const double* __restrict__ emb, const double* __restrict__ q, int N, int d,
+                   double* __restrict__ sim, double* __restrict__ bnd) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* qs = reinterpret_cast<double*>(smem);
+    double* part = qs + d;  // [EPB][WPE][4]
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the select kernel may start its prologue
+    for (int j = threadIdx.x; j < d; j += blockDim.x) qs[j] = q[j];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int eg = warp / kCosWPE, wq = warp % kCosWPE;
+    const int span = d / kCosWPE;  // doubles per warp (even: d % 8 == 0)
+    const double gam = 4.0 * (double)(d + 4) * kU;
+    for (int e0 = blockIdx.x * kCosEPB; e0 < N; e0 += gridDim.x * kCosEPB) {
+        const int e = e0 + eg;
+        double num = 0, na = 0, nb = 0, sab = 0;
+        if (e < N) {
+            const double* a = emb + (int64_t)e * d + wq * span;
+            const double* qq = qs + wq * span;
+            for (int j0 = 2 * lane; j0 < span; j0 += 64 * 8) {
+                double2 av[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + 64 * u;
+                    av[u] = j < span ? __ldg(reinterpret_cast<const double2*>(a + j)) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = j0 + 64 * u;
+                    const double2 qv = j < span ? *reinterpret_cast<const double2*>(qq + j) : make_double2(0.0, 0.0);
+                    num = fma(av[u].x, qv.x, num); num = fma(av[u].y, qv.y, num);
+                    na = fma(av[u].x, av[u].x, na); na = fma(av[u].y, av[u].y, na);
+                    nb = fma(qv.x, qv.x, nb); nb = fma(qv.y, qv.y, nb);
+                    sab += fabs(av[u].x * qv.x) + fabs(av[u].y * qv.y);
+                }
+            }
+            num = warp_sum(num); na = warp_sum(na); nb = warp_sum(nb); sab = warp_sum(sab);
+        }
+        if (lane == 0) {
+            double* pp = part + (eg * kCosWPE + wq) * 4;
+            pp[0] = num; pp[1] = na; pp[2] = nb; pp[3] = sab;
+        }
+        __syncthreads();
+        if (wq == 0 && lane == 0 && e < N) {
+            const double* pp = part + eg * kCosWPE * 4;
+            double tn = 0, ta = 0, tb = 0, ts = 0;
+            for (int w = 0; w < kCosWPE; ++w) {
+                tn += pp[4 * w]; ta += pp[4 * w + 1]; tb += pp[4 * w + 2]; ts += pp[4 * w + 3];
+            }
+            const double den = sqrt(ta) * sqrt(tb);
+            const double sv = tn / den;
+            sim[e] = sv;
+            double b = 2.0 * gam * (ts / den + fabs(sv)) * 1.0000001 + 1e-300;
+            if (!(den > 1e-150)) b = INFINITY;  // tiny/zero norms: always recompute
+            bnd[e] = b;
+        }
+        __syncthreads();
+    }
+}
+
 // reference-order cosine (pattern_cache.hpp:40-46)
 __device__ double ref_cosine(const double* __restrict__ a, const double* __restrict__ b, int d) {
     double num = 0, na = 0, nb = 0;
@@ -101,6 +166,8 @@ k_retrieve_select(const double* __restrict__ sim, const double* __restrict__ bnd
     __shared__ int s_band[kRetThreads];
     __shared__ double s_val[kRetThreads];
     __shared__ int s_cnt;
+    // launched as a programmatic dependent of the scan: the sims are complete here
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // 1) max over fast sims (NaN -> -inf) and the global bound
     double m = -INFINITY, e = 0.0;
     for (int i = threadIdx.x; i < N; i += kRetThreads) {
@@ -216,7 +283,19 @@ void launch_cosine_scan(const double* emb, const double* q, int N, int d, double
                         cudaStream_t st) {
     once_per_device(reinterpret_cast<const void*>(&k_cosine_scan), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_cosine_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_cosine_scan_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     });
+    static const int wide_env = [] {
+        const char* e = getenv("PG_COS_WIDE");
+        return e ? atoi(e) : 1;
+    }();
+    if (wide_env && d % 8 == 0) {
+        const int blocks = min((N + kCosEPB - 1) / kCosEPB, kNumSMs * 8);
+        k_cosine_scan_wide<<<blocks, kCosWPE * kCosEPB * 32, (size_t)d * 8 + kCosEPB * kCosWPE * 32, st>>>(
+            emb, q, N, d, sim, bnd);
+        PG_LAUNCH_CHECK();
+        return;
+    }
     int blocks = min((N + kCosWarps - 1) / kCosWarps, kNumSMs * 2);
     k_cosine_scan<<<blocks, kCosWarps * 32, (size_t)d * 8, st>>>(emb, q, N, d, sim, bnd);
     PG_LAUNCH_CHECK();
@@ -226,9 +305,18 @@ void launch_retrieve_select(const double* sim, const double* bnd, const double* 
                             const double* q, int N, int d, double min_sim, int exact_similarity,
                             double* out_f64, int32_t* out_i32, int32_t* entry_dev,
                             int32_t* hit_dev, cudaStream_t st) {
-    k_retrieve_select<<<1, kRetThreads, 0, st>>>(sim, bnd, emb, q, N, d, min_sim, exact_similarity,
-                                                 out_f64, out_i32, entry_dev, hit_dev);
-    PG_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(kRetThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_retrieve_select, sim, bnd, emb, q, N, d, min_sim, exact_similarity,
+                                     out_f64, out_i32, entry_dev, hit_dev));
+    count_launch();
 }
 
 void launch_cosine_exact(const double* a, const double* b, int d, double* out, cudaStream_t st) {
