@@ -219,6 +219,18 @@ def build_stack(pg, torch, dev, prompts, layers):
     return stack, ldims
 
 
+def config4_config(layers, prompts_per_gpu, world, scaling):
+    """The config-4 workload description, identical in both arms (ours and
+    --impl reference): what is computed, not how."""
+    glob = N_PROMPTS if scaling == "strong" else prompts_per_gpu * world
+    return {"workload": f"config4: {layers}-layer LLaMA-7B-shaped stack of rank-expert linears (q/k/v/o 4096x4096, "
+                        f"gate/up 4096->11008, down 11008->4096) ratio {RATIO}, one decode token for each of "
+                        f"{prompts_per_gpu} heterogeneous prompts per GPU, each prompt with its own expert subset per "
+                        f"linear (reference pattern generator, seed 17171)",
+            "global_batch": glob, "prompts_per_gpu": prompts_per_gpu, "layers": layers,
+            "parallelism": f"dp{world} ({scaling} scaling; replicated weights, no collective)"}
+
+
 def config4_arm(args, rank, world, local_rank):
     import torch
     import paper_2605_08568_b200 as pg
@@ -327,13 +339,9 @@ def config4_arm(args, rank, world, local_rank):
         "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init rank-expert factors and inputs, seeded; selections from the reference's "
                 "pattern generator)",
-        "config": {"workload": f"config4: {args.layers}-layer LLaMA-7B-shaped stack of rank-expert linears "
-                               f"(q/k/v/o 4096x4096, gate/up 4096->11008, down 11008->4096) ratio {RATIO}, decode "
-                               f"batch of {Pl} heterogeneous prompts per GPU, each with its own expert subset per "
-                               f"linear (union-masked tcgen05 GEMMs, q/k/v and up/gate grouped per stage, the "
-                               f"whole step one persistent launch: k_union_prog)",
-                   "global_batch": glob_tok, "prompts_per_gpu": Pl, "layers": args.layers,
-                   "parallelism": f"dp{world} ({args.scaling} scaling; replicated weights, no collective)",
+        "config": config4_config(args.layers, Pl, world, args.scaling),
+        "method": {"kernel": "union-masked tcgen05 GEMMs, q/k/v and up/gate grouped per stage, the whole step one "
+                             "persistent launch (k_union_prog)",
                    "l2": f"{args.layers} distinct layer weight sets, {bytes_step / 1e9:.2f} GB streamed per step "
                          f"(>> 126 MB L2, no flush needed)",
                    "median_ms_per_step": ms_med, "graph": "one CUDA graph per step, replayed"},
@@ -860,10 +868,10 @@ def main():
                 "warmup": args.warmup, "ms_per_step": N_PROMPTS / ref["value"] * 1e3,
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",
-                "config": {"workload": f"config4: {N_LAYERS}-layer LLaMA-7B-shaped rank-expert stack, decode, "
-                                       f"heterogeneous prompts (reference CPU ExecEngine<float>: aggregate_layout + "
-                                       f"aggregated_forward<float>, exec_engine.hpp:112-236)",
-                           "global_batch": N_PROMPTS},
+                "config": config4_config(N_LAYERS, N_PROMPTS // world if args.scaling == "strong" else N_PROMPTS,
+                                         world, args.scaling),
+                "method": {"kernel": "reference CPU ExecEngine<float>: aggregate_layout + aggregated_forward<float> "
+                                     "(exec_engine.hpp:112-236), compiled from /root/reference (oracle/_ref)"},
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
                                                      "nproc", "extrapolated", "ms_per_layer_per_prompt")},
                 "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
