@@ -575,8 +575,14 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
 
     have_dev_pack = hasattr(pg, "pack_selected")
 
-    def pack_all():
-        return {nm: pg.pack_selected(layers[nm][0], sels[nm]) for nm in LIN} if have_dev_pack else None
+    bufs = {}
+
+    def pack_all():  # device pack into persistent buffers (no allocation inside the timed region)
+        if not have_dev_pack:
+            return None
+        for nm in LIN:
+            bufs[nm] = pg.pack_selected(layers[nm][0], sels[nm], into=bufs.get(nm))
+        return dict(bufs)
 
     def gemms(packs):
         for nm in LIN:

@@ -719,9 +719,11 @@ class PackedExperts:
         self.layer, self.k, self.P, self.bt, self.a = layer, k, n_prompts, bt, a
 
 
-def pack_selected(layer: FactorizedLayer, sel: torch.Tensor) -> PackedExperts:
+def pack_selected(layer: FactorizedLayer, sel: torch.Tensor, into: PackedExperts | None = None) -> PackedExperts:
     """Pack each prompt's selection sel [P, K] (device int32, ascending; the
-    router's output) on the device -- no host round trip, no synchronisation."""
+    router's output) on the device -- no host round trip, no synchronisation.
+    `into`: an earlier pack of the same layer and shape whose buffers are
+    reused (serving loops: no allocation per batch)."""
     if not (isinstance(sel, torch.Tensor) and sel.is_cuda):
         raise ValueError("pack_selected: device selection tensor [P, K] expected")
     if sel.dim() == 1:
@@ -730,8 +732,13 @@ def pack_selected(layer: FactorizedLayer, sel: torch.Tensor) -> PackedExperts:
     P, k = sel.shape
     bb, ab = C.c_size_t(), C.c_size_t()
     call("pg_pack_bytes", layer.handle, k, P, C.byref(bb), C.byref(ab))
-    bt = torch.empty(bb.value, dtype=torch.uint8, device=sel.device)
-    a = torch.empty(ab.value, dtype=torch.uint8, device=sel.device)
+    if into is not None:
+        if into.layer is not layer or into.bt.numel() != bb.value or into.a.numel() != ab.value:
+            raise ValueError("pack_selected: `into` packs another layer / shape")
+        bt, a = into.bt, into.a
+    else:
+        bt = torch.empty(bb.value, dtype=torch.uint8, device=sel.device)
+        a = torch.empty(ab.value, dtype=torch.uint8, device=sel.device)
     call("pg_pack_selected", layer.handle, _ptr(sel), k, P, _ptr(bt), _ptr(a), _stream())
     return PackedExperts(layer, k, P, bt, a)
 
