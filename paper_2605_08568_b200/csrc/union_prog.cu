@@ -67,7 +67,11 @@ constexpr int UP_MAXG = 4;
 constexpr int UP_POLL_NS = 100;  // back-off between polls of a dependency counter
 constexpr int UP_CSTRIDE = 32;   // ready counters one per 128-byte line
 constexpr int UP_RED_UNROLL = 3;  // LSU reduction: participants' loads in flight per batch
-constexpr int UP_STG_BYTES = 2 * 32 * WM_BM * 4;  // epilogue staging: 2 x [32 tokens][128 rows] f32 (partial drain)
+#ifndef UP_STG_BUFS_CFG
+#define UP_STG_BUFS_CFG 2
+#endif
+constexpr int UP_STG_BUFS = UP_STG_BUFS_CFG;  // partial-drain bulk stores in flight (2 or 4)
+constexpr int UP_STG_BYTES = UP_STG_BUFS * 32 * WM_BM * 4;  // epilogue staging: [32 tokens][128 rows] f32 buffers
 static_assert(UP_STG_BYTES >= UP_EPI_WARPS * WM_STG_BYTES, "whole-tile staging must fit");
 // [align slack][ring][barriers + slots, 1 KB][token -> pattern table, 1 KB][epilogue staging]
 constexpr int UP_SMEM = 1024 + UP_STAGES * UP_STAGE_BYTES + 1024 + WM_TMAX * 4 + UP_STG_BYTES;
@@ -140,10 +144,11 @@ __device__ __forceinline__ void up_epi_partial_bulk(int Tp, uint32_t taddr, floa
     const bool lead = (et & 127) == 0;
     uint32_t ra[32];
     for (int c = h; c < nch; c += UP_EPI_H) {
-        const int bi = UP_EPI_H == 2 ? h : (c & 1);
+        const int bi = UP_EPI_H == 2 ? h : (c % UP_STG_BUFS);
         float* b = buf + bi * (32 * WM_BM);
-        if (lead && c >= 2) {
+        if (lead && c >= (UP_EPI_H == 2 ? 2 : UP_STG_BUFS)) {
             if (UP_EPI_H == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            else if (UP_STG_BUFS == 4) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
             else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         }
         up_bar_half(h);  // this half's buffer is free
