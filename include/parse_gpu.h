@@ -257,13 +257,16 @@ int pg_module_forward_union(const pg_layer* layers, const uint8_t* const* masks_
  * x_dev / ys_dev addresses are bound at add time; a module whose x_dev is an
  * earlier module's output consumes it tile by tile.  Every output buffer must
  * be distinct and never overwrite an input of an earlier module (per-layer
- * buffers).  The first pg_union_prog_run allocates the workspace (not
+ * buffers).  tok_offset: this module's T tokens are entries [tok_offset,
+ * tok_offset + T) of the run's token -> pattern table (independent token
+ * groups as separate chains in one program); weights_reused: another chain
+ * reads the same weights soon (keep them in L2 instead of evict-first).  The first pg_union_prog_run allocates the workspace (not
  * capturable); later runs are single launches, capturable in CUDA graphs. */
 typedef struct pg_union_prog_s* pg_union_prog;
 int pg_union_prog_create(pg_union_prog* out, size_t T);
 int pg_union_prog_add_module(pg_union_prog prog, const pg_layer* layers, const uint8_t* const* masks_dev,
                              const size_t* P, size_t n_linears, const void* x_dev, void* const* ys_dev,
-                             pg_dtype y_dtype);
+                             pg_dtype y_dtype, size_t tok_offset, int weights_reused);
 int pg_union_prog_run(pg_union_prog prog, const int32_t* tok_pat_dev, pg_stream stream);
 int pg_union_prog_info(pg_union_prog prog, size_t* phases, size_t* grid);
 int pg_union_prog_destroy(pg_union_prog prog);

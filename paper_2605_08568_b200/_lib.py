@@ -89,7 +89,7 @@ _SIGS = {
     "pg_masked_forward_union": [_vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],
     "pg_module_forward_union": [_vp, _vp, _vp, _sz, _vp, _sz, _vp, _vp, _i, _vp],
     "pg_union_prog_create": [C.POINTER(_vp), _sz],
-    "pg_union_prog_add_module": [_vp, _vp, _vp, _vp, _sz, _vp, _vp, _i],
+    "pg_union_prog_add_module": [_vp, _vp, _vp, _vp, _sz, _vp, _vp, _i, _sz, _i],
     "pg_union_prog_run": [_vp, _vp, _vp],
     "pg_union_prog_info": [_vp, C.POINTER(_sz), C.POINTER(_sz)],
     "pg_union_prog_destroy": [_vp],

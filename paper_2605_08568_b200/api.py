@@ -517,7 +517,13 @@ class UnionProgram:
         self._keep = []  # tensors whose addresses the program holds
         self._P = None
 
-    def add_module(self, layers, batches, x: torch.Tensor, outs) -> None:
+    def add_module(self, layers, batches, x: torch.Tensor, outs, tok_offset: int = 0,
+                   weights_reused: bool = False) -> None:
+        """tok_offset: x's T tokens are entries [tok_offset, tok_offset + T) of
+        run()'s token patterns (independent token groups as separate dependency
+        chains of one program, e.g. two halves of a batch interleaved so one
+        half's split-K tail overlaps the other's streaming); weights_reused:
+        another chain reads the same weights soon (L2 evict-normal)."""
         if len(layers) != len(batches) or not layers or len(outs) != len(layers):
             raise ValueError("union_program: one selection batch and one output per layer")
         for L, b in zip(layers, batches):
@@ -534,7 +540,11 @@ class UnionProgram:
         ms = (C.c_void_p * n)(*[_ptr(b.masks) for b in batches])
         ps = (C.c_size_t * n)(*[b.P for b in batches])
         yp = (C.c_void_p * n)(*[_ptr(y) for y in outs])
-        call("pg_union_prog_add_module", self.handle, hs, ms, ps, n, _ptr(x), yp, ydt)
+        if tok_offset < 0 or tok_offset + self.T > 256:
+            raise ValueError("union_program: token offset + T exceeds 256")
+        call("pg_union_prog_add_module", self.handle, hs, ms, ps, n, _ptr(x), yp, ydt, int(tok_offset),
+             int(bool(weights_reused)))
+        self.ttab = max(getattr(self, "ttab", 0), int(tok_offset) + self.T)
         self._keep += [x, *outs, *batches, *layers]
         P = min(b.P for b in batches)
         self._P = P if self._P is None else min(self._P, P)
@@ -550,8 +560,8 @@ class UnionProgram:
                 raise IndexError("union_program: unknown pattern")
             tp = torch.from_numpy(tpn.astype(np.int32)).cuda()
             self._tp = tp
-        if tp.numel() != self.T:
-            raise ValueError("union_program: one pattern id per token")
+        if tp.numel() != getattr(self, "ttab", self.T):
+            raise ValueError("union_program: one pattern id per token of the program")
         call("pg_union_prog_run", self.handle, _ptr(tp), _stream())
 
     def info(self) -> tuple[int, int]:

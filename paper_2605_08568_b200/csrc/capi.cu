@@ -1069,7 +1069,8 @@ int pg_union_prog_create(pg_union_prog* out, size_t T) {
 }
 
 int pg_union_prog_add_module(pg_union_prog H, const pg_layer* Ls, const uint8_t* const* masks, const size_t* Ps,
-                             size_t nlin, const void* x, void* const* ys, pg_dtype ydt) {
+                             size_t nlin, const void* x, void* const* ys, pg_dtype ydt, size_t tok_off,
+                             int weights_reused) {
     PG_API_BEGIN
     require(H && Ls && masks && Ps && x && ys && nlin >= 1 && nlin <= 4, PG_INVALID_ARGUMENT,
             "union_prog_add_module: bad arguments (1..4 linears)");
@@ -1092,8 +1093,12 @@ int pg_union_prog_add_module(pg_union_prog H, const pg_layer* Ls, const uint8_t*
         const pg_layer L = Ls[l];
         const int rp = (int)round_up((size_t)L->r, 8);
         void* zl = static_cast<char*>(z) + zoff[l];
-        s1.push_back(WmSpec{L->bt, L->ldb, L->r, L->n, x, L->n, zl, rp, 1, masks[l], (long long)sel_mask_ld(L->r)});
-        s2.push_back(WmSpec{L->a, L->lda, L->m, L->r, zl, rp, ys[l], L->m, ydt == PG_BF16 ? 1 : 0});
+        WmSpec a{L->bt, L->ldb, L->r, L->n, x, L->n, zl, rp, 1, masks[l], (long long)sel_mask_ld(L->r)};
+        WmSpec b{L->a, L->lda, L->m, L->r, zl, rp, ys[l], L->m, ydt == PG_BF16 ? 1 : 0};
+        a.tok_off = b.tok_off = (int)tok_off;
+        a.w_hint = b.w_hint = weights_reused ? 0 : 1;
+        s1.push_back(a);
+        s2.push_back(b);
     }
     H->prog->add_phase(s1);
     H->prog->add_phase(s2);

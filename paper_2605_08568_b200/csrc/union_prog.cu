@@ -93,6 +93,8 @@ struct __align__(128) UpRec {
     int ready_idx;        // the tile's ready counter (rank 0 half; + rank)
     int flag_base;        // the phase's partial flags [pairs][2]
     int last_in_phase;    // last piece of this pair in its phase
+    int tok_off;          // the GEMM's tokens in the launch's pattern table
+    int w_hint;           // weight loads: 1 evict-first, 0 evict-normal (read again soon by another chain)
 };
 
 struct UpParams {
@@ -101,6 +103,7 @@ struct UpParams {
     const int* pair_off;       // [pairs + 1] record ranges
     const unsigned* pair_tot;  // [pairs][2] partial-slot reads per launch, per parity set
     int T, Tp;
+    int Ttab;                  // token -> pattern table entries (max tok_off + T over the GEMMs)
     const int32_t* tok_pat;
     unsigned* ready;
     const uint8_t* ready_exp;  // writers per launch of each ready counter
@@ -233,8 +236,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
     if (warp == 0) {
         // ------------------------------------------------ weight producer (both CTAs)
         if (lane == 0) {
-            uint64_t pfirst;
+            uint64_t pfirst, pnorm;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pfirst));
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pnorm));
             int s = 0, issued = 0, lastf = -1;
             uint32_t ph = 0;
             for (int i = r0; i < r1; ++i) {
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                     if (issued >= UP_STAGES) u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
                     const uint32_t fb = leader_addr(u_smem(&full[s]));
                     if (leader) u_mbar_arrive_tx_cluster(fb, 2u * WM_W_BYTES);
-                    u_tma_2d_pair_h(u_smem(base + s * UP_STAGE_BYTES), wm, kb * WM_BK, row, fb, pfirst);
+                    u_tma_2d_pair_h(u_smem(base + s * UP_STAGE_BYTES), wm, kb * WM_BK, row, fb, R.w_hint ? pfirst : pnorm);
                     if (f != lastf && f < 8) UP_STAMP(49 + f);
                     lastf = f;
                     if (++s == UP_STAGES) { s = 0; ph ^= 1; }
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
         const int q = warp & 3, h = (warp - 3) >> 2;  // TMEM lane quadrant; half (chunk interleave)
         float* stg = reinterpret_cast<float*>(stage) + (warp - 3) * (WM_STG_BYTES / 4);
         asm volatile("griddepcontrol.wait;" ::: "memory");  // outputs may still be read by the previous kernel
-        for (int t = et; t < P.T; t += UP_EPI_T) tps[t] = P.tok_pat ? __ldg(P.tok_pat + t) : 0;
+        for (int t = et; t < P.Ttab; t += UP_EPI_T) tps[t] = P.tok_pat ? __ldg(P.tok_pat + t) : 0;
         // reads of this pair's partial slots per launch, per parity set: a writer
         // waits for all readers of the slot's previous use before reusing it
         const unsigned tot[2] = {P.pair_tot[pair * 2], P.pair_tot[pair * 2 + 1]};
@@ -348,7 +352,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             const uint32_t taddr = tmem + (uint32_t)(acc * WM_TMAX) + ((uint32_t)(q * 32) << 16);
             if (!R.split) {
                 const UpOut G{R.out, R.ldo, R.out_bf16, R.mask, R.mask_ld, R.Rs};
-                wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps, stg, lane, h, UP_EPI_H);
+                wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps + R.tok_off, stg, lane, h,
+                              UP_EPI_H);
             } else {
                 up_epi_partial_bulk(P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
                                     h, reinterpret_cast<float*>(stage), lane, et);
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 void* const sout = S.out;
                 const uint8_t* const smask = S.mask;
                 const long long sldo = S.ldo, smask_ld = S.mask_ld;
-                const int sRs = S.Rs, sbf16 = S.out_bf16, sflags = S.flag_base, sready = S.ready_idx;
+                const int sRs = S.Rs, sbf16 = S.out_bf16, sflags = S.flag_base, sready = S.ready_idx, stok = S.tok_off;
                 const int row0 = S.row0 + (int)rank * WM_BM;
                 // token slice of this participant, 4-aligned (float4 along tokens)
                 const int ta = me * (P.Tp / 4) / n * 4, tb = min(P.T, (me + 1) * (P.Tp / 4) / n * 4);
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                         mw[j] = 0xFFFFFFFFu;
                         if (smask && tl < ct)
                             mw[j] = __ldg(reinterpret_cast<const uint32_t*>(
-                                smask + (long long)tps[ta + ch * 32 + tl] * smask_ld + row0 + 4 * c4));
+                                smask + (long long)tps[stok + ta + ch * 32 + tl] * smask_ld + row0 + 4 * c4));
                     }
 #pragma unroll
                     for (int j = 0; j < UP_RED_E; ++j) {
@@ -518,6 +523,7 @@ struct HGroup {  // host metadata of one GEMM
     const uint8_t* mask;
     long long mask_ld;
     int src_ready;
+    int tok_off, w_hint;
 };
 struct HPhase {
     int g0, ng, TT, full, rem, ready_base, flag_base;
@@ -546,7 +552,7 @@ static UpGroup* alloc_maps(size_t n) {
 }
 
 struct UnionProgram::Impl {
-    int T = 0, Tp = 0, pairs = 0;
+    int T = 0, Tp = 0, pairs = 0, ttab = 0;
     int dev = 0;
     std::vector<UpGroup> groups;  // device tensor maps
     std::vector<HGroup> hg;
@@ -611,6 +617,11 @@ void UnionProgram::add_phase(const std::vector<WmSpec>& specs) {
         G.out_bf16 = s.out_bf16;
         G.mask = s.mask;
         G.mask_ld = s.mask_ld;
+        if (s.tok_off < 0 || s.tok_off + I.T > WM_TMAX)
+            throw Error{PG_INVALID_ARGUMENT, "union_program: token offset + T exceeds the 256-entry pattern table"};
+        G.tok_off = s.tok_off;
+        G.w_hint = s.w_hint;
+        I.ttab = std::max(I.ttab, s.tok_off + I.T);
         UpGroup M{};
         M.wmap = make_map(s.w, s.R, s.K, s.ldw, WM_BM);
         M.xmap = make_map(s.x, I.T, s.K, s.ldx, I.Tp / 2);
@@ -707,6 +718,8 @@ void UnionProgram::finalize(cudaStream_t st) {
         R.src_ready = G.src_ready;
         R.ready_idx = ph.ready_base + 2 * (G.tile_base + t);
         R.flag_base = ph.flag_base;
+        R.tok_off = G.tok_off;
+        R.w_hint = G.w_hint;
         return R;
     };
     for (int pair = 0; pair < np; ++pair) {
@@ -772,6 +785,7 @@ void UnionProgram::finalize(cudaStream_t st) {
     P.pair_tot = reinterpret_cast<const unsigned*>(I.ws + o_tot);
     P.T = I.T;
     P.Tp = I.Tp;
+    P.Ttab = I.ttab;
     P.epoch = reinterpret_cast<unsigned long long*>(I.ws);
     P.ready = reinterpret_cast<unsigned*>(I.ws + o_ready);
     P.ready_exp = reinterpret_cast<const uint8_t*>(I.ws + o_exp);

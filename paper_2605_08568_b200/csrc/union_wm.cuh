@@ -23,6 +23,8 @@ struct WmSpec {
     int out_bf16;
     const uint8_t* mask = nullptr;
     long long mask_ld = 0;
+    int tok_off = 0;   // union program: this GEMM's token 0 is token tok_off of the launch's pattern table
+    int w_hint = 1;    // union program: L2 policy of the weight loads (1 evict-first, 0 evict-normal)
 };
 
 bool union_wm_enabled();                                 // PG_UNION_WM (default 1)

@@ -172,3 +172,40 @@ def test_union_program_f32_out_and_errors(pg):
         prog2.add_module([lay["o"][0]], [lay["o"][1]], o, [x])
     with pytest.raises(IndexError):
         prog2.run([P] * T)
+
+
+def test_union_program_token_groups(pg):
+    """Two independent token groups as separate dependency chains of one
+    program (tok_offset): each group's rows equal a single-chain program over
+    the whole batch within accumulation order (the split schedules differ)."""
+    D, F, T, P = 512, 1024, 128, 16
+    dims = {nm: (300, 150) for nm in ("q", "k", "v", "o")}
+    dims.update({"up": (700, 350), "gate": (700, 350), "down": (640, 320)})
+    stack, shapes = build(pg, D, F, dims, 2, P, seed=21)
+    pid = torch.from_numpy(np.random.default_rng(9).integers(0, P, T).astype(np.int32)).cuda()
+    x = torch.randn(T, D, device="cuda", generator=torch.Generator(device="cuda").manual_seed(8)).to(torch.bfloat16)
+    prog, bufs = program(pg, stack, shapes, x, T)
+    prog.run(pid)
+    half = T // 2
+    prog2 = pg.UnionProgram(half)
+    bufs2 = []
+    src = x
+    for lay in stack:
+        b = {"x": src}
+        for grp in GROUPS:
+            for nm in grp:
+                b[nm] = torch.empty(T, shapes[nm][0], device="cuda", dtype=torch.bfloat16)
+            for c in range(2):
+                rows = slice(c * half, (c + 1) * half)
+                prog2.add_module([lay[nm][0] for nm in grp], [lay[nm][1] for nm in grp], b[SRC[grp[0]]][rows],
+                                 [b[nm][rows] for nm in grp], tok_offset=c * half, weights_reused=c == 0)
+        bufs2.append(b)
+        src = b["down"]
+    prog2.run(pid)
+    torch.cuda.synchronize()
+    for lay, b in zip(stack, bufs2):
+        for nm in LIN:
+            assert rel(b[nm].float(), module_ref(lay, nm, b[SRC[nm]], pid.long())) <= TOL_BF16_OUT, nm
+    assert rel(bufs2[-1]["down"].float(), bufs[-1]["down"].float()) <= 2e-2
+    with pytest.raises(ValueError):
+        prog2.run(pid[:half])  # one pattern id per token of the program (2 groups)

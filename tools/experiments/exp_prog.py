@@ -17,7 +17,9 @@ T = 256
 stack, ldims = bench.build_stack(pg, torch, dev, list(range(T)), layers)
 tp = torch.arange(T, device=dev, dtype=torch.int32)
 x = torch.randn(T, bench.D_MODEL, device=dev).to(torch.bfloat16)
-prog = pg.UnionProgram(T)
+CH = int(os.environ.get("EXP_CHAINS", "1"))  # independent token groups interleaved as separate chains
+Tc = T // CH
+prog = pg.UnionProgram(Tc)
 bufs = []
 src = x
 for lay in stack:
@@ -25,7 +27,10 @@ for lay in stack:
     for grp in bench.GROUPS:
         for nm in grp:
             b[nm] = torch.empty(T, bench.LIN[nm][0], device=dev, dtype=torch.bfloat16)
-        prog.add_module([lay[nm][0] for nm in grp], [lay[nm][1] for nm in grp], b[bench.SRC[grp[0]]], [b[nm] for nm in grp])
+        for c in range(CH):
+            rows = slice(c * Tc, (c + 1) * Tc)
+            prog.add_module([lay[nm][0] for nm in grp], [lay[nm][1] for nm in grp], b[bench.SRC[grp[0]]][rows],
+                            [b[nm][rows] for nm in grp], tok_offset=c * Tc, weights_reused=(c + 1 < CH))
     bufs.append(b)
     src = b["down"]
 st = torch.cuda.Stream()
