@@ -321,6 +321,54 @@ def config4_arm(args, rank, world, local_rank):
         graphs[False][0].replay()
     st.synchronize()
     agree = float((y_dev.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+    # native fixed-rank SVD on the GPU (north star): the same 32-layer step with
+    # every linear's static prefix y = A[:, :K] (B[:, :K]^T x) through cuBLAS
+    # (torch.matmul, bf16), one selection for all prompts, K experts read
+    # (contiguous copies, K padded to a multiple of 8 with zero experts so every
+    # row is 16-byte aligned for cuBLAS)
+    svd = {}
+    fixed = []
+    for lay in stack:
+        fl = {}
+        for nm in LIN:
+            L = lay[nm][0]
+            bt, a = L._keep
+            K = L.K
+            K8 = (K + 7) // 8 * 8
+            bK = torch.zeros(K8, bt.shape[1], device=dev, dtype=bt.dtype)
+            bK[:K] = bt[:K]
+            aK = torch.zeros(a.shape[0], K8, device=dev, dtype=a.dtype)
+            aK[:, :K] = a[:, :K]
+            fl[nm] = (bK, aK)
+        fixed.append(fl)
+
+    def svd_step():
+        for fl, b in zip(fixed, bufs):
+            h = {"x": b["x"]}
+            for nm in LIN:
+                bK, aK = fl[nm]
+                h[nm] = torch.matmul(torch.matmul(h[SRC[nm]], bK.t()), aK.t())
+            svd["y"] = h["down"]
+
+    with torch.cuda.stream(st):
+        svd_step()
+    st.synchronize()
+    gsvd = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gsvd, stream=st):
+        svd_step()
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            gsvd.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(10):
+            gsvd.replay()
+        e1.record(st)
+    st.synchronize()
+    ms_svd = max_over_ranks(torch, e0.elapsed_time(e1) / 10, dev, world)
+    svd_bytes = args.layers * sum(ldims[i][1] * (m + n) * 2 for i, (m, n) in enumerate(LIN.values()))
+    del gsvd, svd, fixed
+    torch.cuda.empty_cache()
     dom = {"what": "k_union_prog: the whole step (all 32 x 8 union GEMM stages) is one launch",
            "modules_ms_per_step": ms_modules, "modules_launches_per_step": graphs["modules"][1],
            "program_vs_modules_rel": agree}
@@ -355,6 +403,13 @@ def config4_arm(args, rank, world, local_rank):
                                "expert bytes r_store(m+n)*2 of every linear, read once per step for the whole batch",
                      "alg_bytes_per_step": bytes_step, "tensor_tflops": flops_step / step_s / 1e12,
                      "peak_kind": peak_kind, "dominant_launch": dom},
+        "baselines": {"native_fixed_rank_svd_cublas": {
+            "tokens_per_s": glob_tok / (ms_svd * 1e-3), "ms_per_step": ms_svd,
+            "what": "the same 32-layer step with each linear's static prefix A[:, :K] (B[:, :K]^T x) through cuBLAS "
+                    "(torch.matmul, bf16, CUDA graph, contiguous factors with K padded to a multiple of 8): one "
+                    "fixed K-expert subset for every prompt, K(m+n)*2 bytes "
+                    f"per linear ({svd_bytes / 1e9:.2f} GB per step) -- the rank-expert step serves a different subset "
+                    "per prompt and reads the union of the subsets (r_store = 2K experts)"}},
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "clocks": clk.summary(),
