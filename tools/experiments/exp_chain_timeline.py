@@ -34,9 +34,9 @@ a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
 names = {0: "start", 6: "x staged", 1: "ph0 start", 2: "ph0 s1 done", 4: "ph0 z staged", 5: "ph0 s2 done",
          7: "ph1 start", 14: "ph1 s1 data", 8: "ph1 s1 done", 10: "ph1 z staged", 11: "ph1 s2 done",
-         12: "producer done", 13: "end"}
+         12: "producer done", 13: "end", 15: "ph1 s2 data"}
 print(f"CTAs {a.shape[0]}")
-for k in (0, 6, 1, 2, 4, 5, 7, 14, 8, 10, 11, 12, 13):
+for k in (0, 6, 1, 2, 4, 5, 7, 14, 8, 10, 15, 11, 12, 13):
     v = a[:, k]
     v = (v[v > 0] - t0) / 1e3
     if v.size:
