@@ -366,9 +366,55 @@ def config4_arm(args, rank, world, local_rank):
         e1.record(st)
     st.synchronize()
     ms_svd = max_over_ranks(torch, e0.elapsed_time(e1) / 10, dev, world)
-    svd_bytes = args.layers * sum(ldims[i][1] * (m + n) * 2 for i, (m, n) in enumerate(LIN.values()))
-    del gsvd, svd, fixed
+    del gsvd, fixed
     torch.cuda.empty_cache()
+    # the same union-masked step through cuBLAS: per linear Z = X B^T over all
+    # r_store experts (torch.matmul), the per-token selection mask as a torch
+    # multiply (bf16), Y = Z A^T -- identical GEMM shapes and bytes to k_union_prog
+    # (operands copied with r_store padded to a multiple of 8 by zero experts, so
+    # every row is 16-byte aligned for cuBLAS, as the kernel pads Z)
+    umask = []
+    for lay in stack:
+        um = {}
+        for nm in LIN:
+            L, sb = lay[nm][0], lay[nm][1]
+            r8 = (L.r_store + 7) // 8 * 8
+            bt, a = L._keep
+            bp = torch.zeros(r8, bt.shape[1], device=dev, dtype=bt.dtype)
+            bp[:L.r_store] = bt
+            ap = torch.zeros(a.shape[0], r8, device=dev, dtype=a.dtype)
+            ap[:, :L.r_store] = a
+            mk = torch.zeros(len(prompts), r8, device=dev, dtype=torch.bfloat16)
+            mk[:, :L.r_store] = sb.masks.view(sb.P, sb.stride)[:, :L.r_store].to(torch.bfloat16)[tp.long()]
+            um[nm] = (bp, ap, mk)
+        umask.append(um)
+
+    def cublas_union_step():
+        for um, b in zip(umask, bufs):
+            h = {"x": b["x"]}
+            for nm in LIN:
+                bp, ap, mk = um[nm]
+                h[nm] = torch.matmul(torch.matmul(h[SRC[nm]], bp.t()) * mk, ap.t())
+            svd["u"] = h["down"]
+
+    with torch.cuda.stream(st):
+        cublas_union_step()
+    st.synchronize()
+    gcu = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gcu, stream=st):
+        cublas_union_step()
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            gcu.replay()
+        e0.record(st)
+        for _ in range(10):
+            gcu.replay()
+        e1.record(st)
+    st.synchronize()
+    ms_cu = max_over_ranks(torch, e0.elapsed_time(e1) / 10, dev, world)
+    del gcu, umask
+    svd_bytes = args.layers * sum(ldims[i][1] * (m + n) * 2 for i, (m, n) in enumerate(LIN.values()))
+    del svd
     dom = {"what": "k_union_prog: the whole step (all 32 x 8 union GEMM stages) is one launch",
            "modules_ms_per_step": ms_modules, "modules_launches_per_step": graphs["modules"][1],
            "program_vs_modules_rel": agree}
@@ -403,7 +449,12 @@ def config4_arm(args, rank, world, local_rank):
                                "expert bytes r_store(m+n)*2 of every linear, read once per step for the whole batch",
                      "alg_bytes_per_step": bytes_step, "tensor_tflops": flops_step / step_s / 1e12,
                      "peak_kind": peak_kind, "dominant_launch": dom},
-        "baselines": {"native_fixed_rank_svd_cublas": {
+        "baselines": {"union_gemms_cublas": {
+            "tokens_per_s": glob_tok / (ms_cu * 1e-3), "ms_per_step": ms_cu,
+            "what": "the identical union-masked step through cuBLAS: per linear torch.matmul over all r_store experts, "
+                    "the per-token selection mask as a bf16 multiply, torch.matmul back (2 GEMMs + 1 elementwise per "
+                    "linear, 7 linears x 32 layers, CUDA graph; operands zero-padded to r_store rounded to 8)"},
+            "native_fixed_rank_svd_cublas": {
             "tokens_per_s": glob_tok / (ms_svd * 1e-3), "ms_per_step": ms_svd,
             "what": "the same 32-layer step with each linear's static prefix A[:, :K] (B[:, :K]^T x) through cuBLAS "
                     "(torch.matmul, bf16, CUDA graph, contiguous factors with K padded to a multiple of 8): one "
@@ -673,6 +724,38 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
         gemms(packs)
     e[3].record()
     barrier(torch, world)
+    # the same packed GEMMs through cuBLAS (torch.bmm over the 16 prompts: the
+    # batched-GEMM analogue of the grouped launch), z rounded to bf16 between
+    cub_ms = None
+    if have_dev_pack:
+        def cublas_gemms():
+            for nm, (m, n) in LIN.items():
+                pk = packs[nm]
+                kp = (pk.k + 7) // 8 * 8
+                ldb = pk.bt.numel() // 2 // (P * kp)
+                bt = pk.bt.view(torch.bfloat16).view(P, kp, ldb)[:, :, :n]
+                a = pk.a.view(torch.bfloat16).view(P, m, kp)
+                x = src[nm].view(P, T, n)
+                z = torch.bmm(x, bt.transpose(1, 2))
+                outs[nm].view(P, T, m).copy_(torch.bmm(z, a.transpose(1, 2)))
+
+        gst = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(gst):
+            cublas_gemms()
+        gst.synchronize()
+        gcb = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gcb, stream=gst):
+            cublas_gemms()
+        ec = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(gst):
+            gcb.replay()
+            ec[0].record(gst)
+            for _ in range(reps):
+                gcb.replay()
+            ec[1].record(gst)
+        gst.synchronize()
+        cub_ms = max_over_ranks(torch, ec[0].elapsed_time(ec[1]) / reps, dev, world)
+        del gcb
     route_ms = max_over_ranks(torch, e[0].elapsed_time(e[1]) / reps, dev, world)
     pack_ms = max_over_ranks(torch, e[1].elapsed_time(e[2]) / reps, dev, world) if have_dev_pack else pack_ms_host
     ms = max_over_ranks(torch, e[2].elapsed_time(e[3]) / reps, dev, world)
@@ -684,6 +767,10 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
            "gemm_tokens_per_s": P * T / (ms * 1e-3) * world,
            "ms_per_layer": ms, "route_ms": route_ms, "pack_ms": pack_ms,
            "pack_on_device": have_dev_pack,
+           "baselines": {"packed_gemms_cublas": None if cub_ms is None else {
+               "ms_per_layer": cub_ms, "tflops": flops / (cub_ms * 1e-3) / 1e12,
+               "what": "the same packed per-prompt GEMMs through cuBLAS (torch.bmm over the 16 prompts, "
+                       "z rounded to bf16 between the stages, CUDA graph)"}},
            "roofline": {"bound": "tensor", "achieved": achieved, "peak": tflops_peak, "unit": "TFLOP/s",
                         "frac": achieved / tflops_peak, "flops_per_layer": flops, "peak_kind": peak_kind,
                         "kernel": "k_umma_grouped2 (tcgen05.mma cta_group::2 kind::f16, TMA, TMEM; 2 grouped "
