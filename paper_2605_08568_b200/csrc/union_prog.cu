@@ -815,16 +815,24 @@ void UnionProgram::run(const int32_t* tok_pat, cudaStream_t st) {
     cfg.blockDim = dim3(UP_THREADS);
     cfg.dynamicSmemBytes = UP_SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    // cooperative: the CTAs wait on each other's output tiles, so the launch must
+    // guarantee that the whole grid is co-resident (it fails instead of hanging)
+    static const int coop = [] {
+        const char* e = getenv("PG_PROG_COOP");
+        return e ? atoi(e) : 1;
+    }();
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
+    at[2].id = cudaLaunchAttributeCooperative;
+    at[2].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
-        PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_union_prog, P));
+    cfg.numAttrs = coop ? 3 : 2;
+    PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_union_prog, P));
     count_launch();
 }
 
