@@ -544,15 +544,18 @@ void launch_union_wm(const std::vector<WmSpec>& specs, int T, const int32_t* tok
     cfg.blockDim = dim3(WM_THREADS);
     cfg.dynamicSmemBytes = WM_SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    // cooperative: split-tile participants wait on each other's partial flags
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
+    at[2].id = cudaLaunchAttributeCooperative;
+    at[2].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = 3;
     PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_union_wm, *P));
     count_launch();
 }
