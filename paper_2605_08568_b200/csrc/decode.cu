@@ -598,10 +598,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         if (!P.ztag) grid_sync_consumers(P.bar);
         if (ph < 2) STAMP(ph * 6 + 3);
         // ---- z into shared memory (inactive slots -> 0)
-        int zoff[kMaxLin];
+        int zoff[kMaxLin] = {0, 0, 0};
         {
             int o = 0;
-            for (int l = 0; l < nlin; ++l) {
+#pragma unroll
+            for (int l = 0; l < kMaxLin; ++l) {  // unrolled: zoff stays in registers
+                if (l >= nlin) break;
                 zoff[l] = o;
                 const unsigned long long* zx = static_cast<const unsigned long long*>(L[l].z);
                 const int ns = L[l].nslots;
@@ -714,7 +716,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                     } else {
                         const int ns = L[l].nslots;
                         const int4* r = reinterpret_cast<const int4*>(base + (size_t)q * ns * es);
-                        const A* z = zs + zoff[l];
+                        // selects, not a dynamic index: keeps zoff in registers (no stack frame)
+                        const A* z = zs + (l == 0 ? zoff[0] : (l == 1 ? zoff[1] : zoff[2]));
                         const int pl = (ns + 7) / 8 * 4;
                         A acc = A(0);
                         if constexpr (sizeof(W) == 2) {

@@ -85,8 +85,10 @@ __device__ __forceinline__ void store_chunk(const UmmaGroup& G, int row, int n0,
                 }
                 *reinterpret_cast<uint4*>(o + v * 8) = w;
             }
-        } else {
-            for (int e = 0; e < valid; ++e) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+        } else {  // unrolled with a predicate: a dynamic index would put r in local memory
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+                if (e < valid) o[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
         }
     } else {
         float* o = static_cast<float*>(G.out) + (long long)row * G.ldo + cb;
@@ -96,7 +98,9 @@ __device__ __forceinline__ void store_chunk(const UmmaGroup& G, int row, int n0,
                 *reinterpret_cast<float4*>(o + v * 4) = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                                                                     __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
         } else {
-            for (int e = 0; e < valid; ++e) o[e] = __uint_as_float(r[e]);
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+                if (e < valid) o[e] = __uint_as_float(r[e]);
         }
     }
 }
@@ -268,6 +272,17 @@ constexpr int U2_STAGE_BYTES = U2_A_BYTES + U2_B_BYTES;
 constexpr int U2_OUT_BYTES = 32 * 32 * 4;  // one 32 x 32 output chunk (f32 worst case)
 // [align slack 1 KB][ring][barriers, 1 KB][per-warp output staging]
 constexpr int U2_SMEM = U2_STAGES * U2_STAGE_BYTES + 1024 + 1024 + 4 * 2 * U2_OUT_BYTES;
+// the CTA-pair kernel (k_umma_grouped2): U2_EPI_WARPS epilogue warps -- with 8,
+// two per TMEM lane quadrant take alternate 32-column chunks (short-K tiles are
+// drain-bound), and the ring gives up a stage for their staging
+#ifndef U2_EPI_WARPS_CFG
+#define U2_EPI_WARPS_CFG 4
+#endif
+constexpr int U2_EPI_WARPS = U2_EPI_WARPS_CFG;
+constexpr int P2_THREADS = 64 + 32 * U2_EPI_WARPS;
+constexpr int P2_STAGES = U2_EPI_WARPS == 8 ? 5 : U2_STAGES;
+constexpr int P2_SMEM = P2_STAGES * U2_STAGE_BYTES + 1024 + 1024 + U2_EPI_WARPS * 2 * U2_OUT_BYTES;
+static_assert(P2_SMEM <= 227 * 1024, "pair kernel shared memory");
 
 // ---- k_umma_grouped4 (PG_UMMA_MC=1, off by default): clusters of two CTA
 // pairs on consecutive M tiles of one N tile; each CTA loads a quarter of the
@@ -299,7 +314,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 }
 __device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUtensorMap* omap, uint32_t tbase, int q,
                                                   int lane, int row0, int n0, unsigned char* stage, int& nbuf,
-                                                  int epi_deep) {
+                                                  int epi_deep, int c0 = 0, int cstep = 1) {
     const int nch = (G.bn + 31) / 32;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const int es = G.out_bf16 ? 2 : 4;
@@ -348,40 +363,41 @@ __device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUte
         }
         ++nbuf;
     };
-    tmem_ld32(lane_base, ra);
-    for (int c = 0; c < nch; c += 2) {
+    if (c0 >= nch) return;
+    tmem_ld32(lane_base + (uint32_t)(32 * c0), ra);
+    for (int c = c0; c < nch; c += 2 * cstep) {
         tmem_wait_ld();
-        if (c + 1 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 1)), rb);
+        if (c + cstep < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + cstep)), rb);
         emit(c, ra);
-        if (c + 1 >= nch) break;
+        if (c + cstep >= nch) break;
         tmem_wait_ld();
-        if (c + 2 < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 2)), ra);
-        emit(c + 1, rb);
+        if (c + 2 * cstep < nch) tmem_ld32(lane_base + (uint32_t)(32 * (c + 2 * cstep)), ra);
+        emit(c + cstep, rb);
     }
 }
 
-__global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_constant__ UmmaParams P) {
+__global__ void __launch_bounds__(P2_THREADS, 1) k_umma_grouped2(const __grid_constant__ UmmaParams P) {
     extern __shared__ __align__(1024) unsigned char usmem[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(usmem) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + U2_STAGES * U2_STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + P2_STAGES * U2_STAGE_BYTES);
     uint64_t* full = bars;                        // [STAGES] (used in the leader)
-    uint64_t* empty = bars + U2_STAGES;           // [STAGES] (each CTA)
-    uint64_t* tfull = bars + 2 * U2_STAGES;       // [2] (each CTA)
-    uint64_t* tempty = bars + 2 * U2_STAGES + 2;  // [2] (used in the leader: both CTAs' epilogues)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * U2_STAGES + 4);
+    uint64_t* empty = bars + P2_STAGES;           // [STAGES] (each CTA)
+    uint64_t* tfull = bars + 2 * P2_STAGES;       // [2] (each CTA)
+    uint64_t* tempty = bars + 2 * P2_STAGES + 2;  // [2] (used in the leader: both CTAs' epilogues)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P2_STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < U2_STAGES; ++s) {
+        for (int s = 0; s < P2_STAGES; ++s) {
             u_mbar_init(u_smem(&full[s]), 1);
             u_mbar_init(u_smem(&empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
             u_mbar_init(u_smem(&tfull[a]), 1);
-            u_mbar_init(u_smem(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
+            u_mbar_init(u_smem(&tempty[a]), 2 * U2_EPI_WARPS);  // epilogue warps x 2 CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -425,7 +441,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
                         u_tma_2d_pair_h(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb,
                                         u_policy(G.b_hint, pf, pl));
                     else u_tma_2d_pair(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
-                    if (++s == U2_STAGES) { s = 0; ph ^= 1; }
+                    if (++s == P2_STAGES) { s = 0; ph ^= 1; }
                 }
             }
         }
@@ -452,7 +468,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
                     for (int k = 0; k < UM_BK / 16; ++k)
                         u_mma2(d, u_desc(sa + k * 32), u_desc(sb + k * 32), idesc, (kb | k) != 0);
                     u_commit2(u_smem(&empty[s]));  // frees the stage in both CTAs
-                    if (++s == U2_STAGES) { s = 0; ph ^= 1; }
+                    if (++s == P2_STAGES) { s = 0; ph ^= 1; }
                 }
                 u_commit2(u_smem(&tfull[acc]));  // accumulator ready in both CTAs
                 if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -460,8 +476,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
         }
     } else {
         // ------------------------------------------------ epilogue (warps 2-5, both CTAs)
-        const int q = warp & 3;
-        unsigned char* ostage = base + U2_STAGES * U2_STAGE_BYTES + 1024 + (q) * 2 * U2_OUT_BYTES;
+        const int q = warp & 3, h = (warp - 2) >> 2;  // TMEM lane quadrant; column-chunk half (8 warps)
+        unsigned char* ostage = base + P2_STAGES * U2_STAGE_BYTES + 1024 + (warp - 2) * 2 * U2_OUT_BYTES;
         int nbuf = 0;
         int acc = 0;
         uint32_t aph = 0;
@@ -474,9 +490,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma_grouped2(const __grid_co
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const int row = m0 + q * 32 + lane;
-            if (G.direct_epi) epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
+            if (G.direct_epi) {
+                if (h == 0) epilogue_tile(G, tmem + (uint32_t)(acc * UM_BN_MAX), q, row, n0);
+            }
             else epilogue_tile_tma(G, &P.omaps[g], tmem + (uint32_t)(acc * UM_BN_MAX), q, lane, m0 + q * 32, n0, ostage, nbuf,
-                                   P.epi_deep);
+                                   P.epi_deep, U2_EPI_WARPS == 8 ? h : 0, U2_EPI_WARPS / 4);
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
@@ -694,7 +712,7 @@ static int umma_pairs_enabled() {
 void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
     once_per_device(reinterpret_cast<const void*>(&k_umma_grouped), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     });
@@ -823,8 +841,8 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             static int max_pairs = [&] {
                 cudaLaunchConfig_t q = {};
                 q.gridDim = dim3((unsigned)(sms / 2 * 2));
-                q.blockDim = dim3(UM_THREADS);
-                q.dynamicSmemBytes = U2_SMEM;
+                q.blockDim = dim3(P2_THREADS);
+                q.dynamicSmemBytes = P2_SMEM;
                 cudaLaunchAttribute a[1];
                 a[0].id = cudaLaunchAttributeClusterDimension;
                 a[0].val.clusterDim.x = 2;
@@ -839,8 +857,8 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             }();
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)(2 * std::min(tiles, max_pairs)));
-            cfg.blockDim = dim3(UM_THREADS);
-            cfg.dynamicSmemBytes = U2_SMEM;
+            cfg.blockDim = dim3(P2_THREADS);
+            cfg.dynamicSmemBytes = P2_SMEM;
             cfg.stream = st;
             cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributeClusterDimension;

@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
         for (int t = et; t < P.Ttab; t += UP_EPI_T) tps[t] = P.tok_pat ? __ldg(P.tok_pat + t) : 0;
         // reads of this pair's partial slots per launch, per parity set: a writer
         // waits for all readers of the slot's previous use before reusing it
-        const unsigned tot[2] = {P.pair_tot[pair * 2], P.pair_tot[pair * 2 + 1]};
-        unsigned used[2] = {0u, 0u};
+        const unsigned tot0 = P.pair_tot[pair * 2], tot1 = P.pair_tot[pair * 2 + 1];
+        unsigned used0 = 0u, used1 = 0u;  // scalars, not arrays indexed by the phase parity (no stack frame)
         up_bar_epi();
         int acc = 0, pi = 0, lastf = -1;
         uint32_t aph = 0;
@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             if (R.split) {
                 red_rec = i;
                 if (et == 0)  // every reader of this slot's previous use is done
-                    wait_count(P.consumed + (set * np + pair) * 2 + rank, (tag - 1u) * tot[set] + used[set]);
+                    wait_count(P.consumed + (set * np + pair) * 2 + rank,
+                               (tag - 1u) * (set ? tot1 : tot0) + (set ? used1 : used0));
             }
             u_mbar_wait(u_smem(&tfull[acc]), aph);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -366,7 +367,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 __threadfence();
                 if (R.split) {
                     st_release(P.flags + R.flag_base + pair * 2 + (int)rank, tag);
-                    used[set] += (unsigned)R.n;
+                    if (set) used1 += (unsigned)R.n;
+                    else used0 += (unsigned)R.n;
                 } else {
                     red_release_add(P.ready + (size_t)(R.ready_idx + (int)rank) * UP_CSTRIDE, 1u);
                 }
