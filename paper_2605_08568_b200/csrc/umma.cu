@@ -673,6 +673,19 @@ CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int box_row
     return m;
 }
 
+CUtensorMap make_store_map(void* ptr, int rows, int cols, long long ld, bool bf16, int box_cols, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * (bf16 ? 2 : 4)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = get_encode()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr,
+                                    dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error{PG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (store map)"};
+    return m;
+}
+
 static CUtensorMap make_out_map(void* ptr, int rows, int cols, long long ld, bool bf16) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};

@@ -47,6 +47,9 @@ bool launch_umma_splitk_multi(const std::vector<UmmaSpec>& specs, void* workspac
 // 2-D bf16 K-major TMA operand map [rows, K] (row stride ld elements), box
 // {64, box_rows}, 128-byte swizzle (the UMMA K-major SW128 layout).
 CUtensorMap make_map(const void* ptr, int rows, int K, long long ld, int box_rows);
+// 2-D output map [rows, cols] (row stride ld elements), box {box_cols, box_rows},
+// no swizzle: TMA-store epilogues (rows / columns past the bounds are clipped).
+CUtensorMap make_store_map(void* ptr, int rows, int cols, long long ld, bool bf16, int box_cols, int box_rows);
 
 // All specs run as grouped launches (<= 32 groups per launch), async on st.
 void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st);

@@ -89,6 +89,6 @@ if os.environ.get("PG_PROG_DBG"):
         v = a[:, k]
         v = (v[v > 0] - t0) / 1e3
         return f"{np.median(v):7.1f}/{v.max():7.1f}" if v.size else "      -/      -"
-    print("phase  W_first      X_first      X_last       epi_p0       epi_all      flags        done   (med/max us)")
+    print("phase  W_first      X_first      X_last       acc0_ready   epi_p0       epi_all      flags        done   (med/max us)")
     for f in range(8):
-        print(f"{names[f]:5s} " + " ".join(col(k) for k in (49 + f, 33 + f, 41 + f, 1 + f, 9 + f, 17 + f, 25 + f)))
+        print(f"{names[f]:5s} " + " ".join(col(k) for k in (49 + f, 33 + f, 41 + f, (57 + f) if f < 7 else 63, 1 + f, 9 + f, 17 + f, 25 + f)))
