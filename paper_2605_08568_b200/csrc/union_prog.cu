@@ -176,71 +176,6 @@ __device__ __forceinline__ void up_epi_partial_bulk(int Tp, uint32_t taddr, floa
 }
 
 constexpr int UP_RED_E = 32 * 32 / UP_EPI_T;  // float4s of a 32-token chunk per epilogue thread
-constexpr int UP_RED_E = 32 * 32 / UP_EPI_T;  // float4s of a 32-token chunk per epilogue thread
-// whole tile, bf16 output: TMEM -> per-warp transpose (f32 [32 tokens][32 rows])
-// -> mask, bf16 -> shared [32 tokens][128 rows] (the 4 warps' rows side by side,
-// 8 KB, double-buffered) -> one TMA store per 32-token chunk: full 256-byte row
-// segments per token instead of scattered 16-byte stores.  The stores are
-// complete (and ordered before the caller's release) on return.
-template <class G_>
-__device__ __forceinline__ void up_epi_direct_tma(int Tp, int T, const G_& G, const CUtensorMap* omap, uint32_t taddr,
-                                                  int row0, int q, int lane, int et, const int32_t* tps, float* stg,
-                                                  __nv_bfloat16* obuf) {
-    const int nch = Tp / 32;
-    const uint8_t* const mask = G.mask;
-    const long long mask_ld = G.mask_ld;
-    uint32_t ra[32];
-    for (int c = 0; c < nch; ++c) {
-        uint2 mw[4];
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int sgi = it * 32 + lane, tok = c * 32 + (sgi >> 2);
-            mw[it] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-            if (mask && tok < T)
-                mw[it] = __ldg(reinterpret_cast<const uint2*>(mask + (long long)tps[tok] * mask_ld + row0 + q * 32 +
-                                                              (sgi & 3) * 8));
-        }
-        tmem_ld32(taddr + 32u * c, ra);
-        tmem_wait_ld();
-        __syncwarp();  // the previous chunk's reads of stg are done
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stg[j * 32 + lane] = __uint_as_float(ra[j]);  // [token][row]
-        __syncwarp();
-        __nv_bfloat16* b = obuf + (c & 1) * (32 * WM_BM);
-        if (et == 0 && c >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        up_bar_epi();  // buffer c & 1 is free
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int sgi = it * 32 + lane, tl = sgi >> 2, part = sgi & 3;
-            const float4 a0 = *reinterpret_cast<const float4*>(stg + tl * 32 + part * 8);
-            const float4 a1 = *reinterpret_cast<const float4*>(stg + tl * 32 + part * 8 + 4);
-            float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (!(((e < 4 ? mw[it].x : mw[it].y) >> (8 * (e & 3))) & 0xFFu)) v[e] = 0.f;
-            uint4 w;
-            uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-                wp[e] = *reinterpret_cast<uint32_t*>(&h2);
-            }
-            *reinterpret_cast<uint4*>(b + tl * WM_BM + q * 32 + part * 8) = w;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        up_bar_epi();  // the chunk is in shared memory
-        if (et == 0) {
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(omap),
-                         "r"(row0), "r"(c * 32), "r"(u_smem(b))
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-    }
-    if (et == 0) {
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-}
 
 struct F4xE {
     float4 v[UP_RED_E];
