@@ -64,9 +64,15 @@ constexpr int UP_EPI_T = 32 * UP_EPI_WARPS;
 constexpr int UP_EPI_H = UP_EPI_WARPS / 4;      // epilogue halves (chunk interleave)
 constexpr int UP_THREADS = 96 + UP_EPI_T;
 constexpr int UP_MAXG = 4;
-constexpr int UP_POLL_NS = 100;  // back-off between polls of a dependency counter
+#ifndef UP_POLL_NS_CFG
+#define UP_POLL_NS_CFG 100
+#endif
+constexpr int UP_POLL_NS = UP_POLL_NS_CFG;  // back-off between polls of a dependency counter
 constexpr int UP_CSTRIDE = 32;   // ready counters one per 128-byte line
-constexpr int UP_RED_UNROLL = 3;  // LSU reduction: participants' loads in flight per batch
+#ifndef UP_RED_UNROLL_CFG
+#define UP_RED_UNROLL_CFG 3
+#endif
+constexpr int UP_RED_UNROLL = UP_RED_UNROLL_CFG;  // LSU reduction: participants' loads in flight per batch
 #ifndef UP_STG_BUFS_CFG
 #define UP_STG_BUFS_CFG 2
 #endif
@@ -112,15 +118,20 @@ struct UpParams {
     float* partial;            // [2][pairs][2][WM_PART_FLOATS]
     unsigned long long* epoch;
     unsigned long long* dbg;
+    int exp;  // PG_PROG_EXP (timing experiments only, wrong results): 1 no reduction loads, 2 no partial drain, 4 no whole-tile stores
 };
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // poll with a short back-off: every CTA of a phase waits on the same few
-// counters, and tight acquire loads from 148 SMs would hammer their L2 lines
+// counters, and tight loads from 148 SMs would hammer their L2 lines.  The
+// polls are relaxed (an acquire load invalidates the SM's L1 each time); one
+// acquire load of the (monotonic) counter after the target is seen orders the
+// caller's later reads.
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
-    while ((int)(ld_acquire(p) - target) < 0) __nanosleep(UP_POLL_NS);
+    while ((int)(ld_relaxed(p) - target) < 0) __nanosleep(UP_POLL_NS);
+    (void)ld_acquire(p);
 }
 __device__ __forceinline__ void up_bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(UP_EPI_T) : "memory"); }
 __device__ __forceinline__ void up_bar_half(int h) { asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory"); }
@@ -171,7 +182,6 @@ __device__ __forceinline__ void up_epi_partial_bulk(int Tp, uint32_t taddr, floa
     if (lead) {
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
     }
 }
 
@@ -353,7 +363,8 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             if (et == 0 && f < 7 && pi == 0) UP_STAMP(57 + f);  // accumulator of the phase's first piece ready
             if (R.split) up_bar_epi();  // the slot wait above
             const uint32_t taddr = tmem + (uint32_t)(acc * WM_TMAX) + ((uint32_t)(q * 32) << 16);
-            if (!R.split) {
+            if (P.exp & (R.split ? 2 : 4)) {
+            } else if (!R.split) {
                 const UpOut G{R.out, R.ldo, R.out_bf16, R.mask, R.mask_ld, R.Rs};
                 wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps + R.tok_off, stg, lane, h,
                               UP_EPI_H);
@@ -365,8 +376,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             __syncwarp();
             if (lane == 0) u_mbar_arrive_cluster(leader_addr(u_smem(&tempty[acc])));
             up_bar_epi();  // every epilogue thread's stores are issued (and the staging is free)
-            if (et == 0) {
-                __threadfence();
+            if (et == 0) {  // the release is cumulative over the epilogue's stores (bar.sync above)
                 if (R.split) {
                     st_release(P.flags + R.flag_base + pair * 2 + (int)rank, tag);
                     if (set) used1 += (unsigned)R.n;
@@ -395,11 +405,26 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 // token slice of this participant, 4-aligned (float4 along tokens)
                 const int ta = me * (P.Tp / 4) / n * 4, tb = min(P.T, (me + 1) * (P.Tp / 4) / n * 4);
                 const int cnt = max(0, tb - ta);
+                // the slice's mask bytes (stage-1 outputs) into the idle staging
+                // buffer while the participants finish: [cnt tokens][128 rows]
+                uint8_t* const msk = stage;
+                if (smask) {
+                    for (int idx = et; idx < cnt * 8; idx += UP_EPI_T) {
+                        const int tl = idx >> 3, part = idx & 7;
+                        if (row0 + part * 16 < sRs)
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(u_smem(msk + tl * 128 + part * 16)),
+                                         "l"(smask + (long long)tps[stok + ta + tl] * smask_ld + row0 + part * 16)
+                                         : "memory");
+                    }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                }
                 if (warp == 3)  // every participant's flag, one lane each
                     for (int pp = pf + lane; pp < pf + n; pp += 32) {
                         const unsigned* fl = P.flags + sflags + pp * 2 + (int)rank;
-                        while (ld_acquire(fl) != tag) __nanosleep(UP_POLL_NS);
+                        while (ld_relaxed(fl) != tag) __nanosleep(UP_POLL_NS);
+                        (void)ld_acquire(fl);
                     }
+                if (smask) asm volatile("cp.async.wait_all;" ::: "memory");
                 up_bar_epi();
                 if (et == 0 && f < 8) UP_STAMP(17 + f);
                 const float* pbase = P.partial + ((size_t)(set * np) * 2 + rank) * WM_PART_FLOATS;
@@ -411,9 +436,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                     for (int j = 0; j < UP_RED_E; ++j) {
                         const int e = et + UP_EPI_T * j, tl = e >> 5, c4 = e & 31;
                         mw[j] = 0xFFFFFFFFu;
-                        if (smask && tl < ct)
-                            mw[j] = __ldg(reinterpret_cast<const uint32_t*>(
-                                smask + (long long)tps[stok + ta + ch * 32 + tl] * smask_ld + row0 + 4 * c4));
+                        if (smask && tl < ct) mw[j] = *reinterpret_cast<const uint32_t*>(msk + (ch * 32 + tl) * 128 + 4 * c4);
                     }
 #pragma unroll
                     for (int j = 0; j < UP_RED_E; ++j) {
@@ -444,7 +467,6 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                     }
                 };
                 {
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     // LSU: per 32-token chunk, UP_RED_E float4 per thread per participant,
                     // three participants' loads in flight at a time, summed in pair order
                     for (int ch = 0; ch * 32 < cnt; ++ch) {
@@ -457,8 +479,9 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                             for (int u = 0; u < UP_RED_UNROLL; ++u)
 #pragma unroll
                                 for (int j = 0; j < UP_RED_E; ++j) {
+                                    v[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
                                     const int e = et + UP_EPI_T * j;
-                                    if (pp + u < n && (e >> 5) < ct)
+                                    if (pp + u < n && (e >> 5) < ct && !(P.exp & 1))
                                         v[u][j] = __ldcg(reinterpret_cast<const float4*>(s0 + (size_t)u * 2 * WM_PART_FLOATS) + e);
                                 }
 #pragma unroll
@@ -474,8 +497,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                     }
                 }
                 up_bar_epi();  // slice stored
-                if (et == 0) {
-                    __threadfence();
+                if (et == 0) {  // cumulative release (bar.sync above)
                     red_release_add(P.ready + (size_t)(sready + (int)rank) * UP_CSTRIDE, 1u);
                 }
                 if (et < n) red_release_add(P.consumed + (set * np + pf + et) * 2 + rank, 1u);
@@ -792,6 +814,8 @@ void UnionProgram::finalize(cudaStream_t st) {
         PG_CUDA_THROW(cudaMemset(I.dbg, 0, (size_t)2 * np * 64 * 8));
     }
     UpParams& P = I.P;
+    const char* ex = getenv("PG_PROG_EXP");
+    P.exp = ex ? atoi(ex) : 0;
     P.groups = I.d_groups;
     P.recs = I.d_recs;
     P.pair_off = reinterpret_cast<const int*>(I.ws + o_off);
