@@ -19,6 +19,9 @@
 #include <algorithm>
 
 #include "chain.cuh"
+#ifndef CHAIN_RELAXED_POLL
+#define CHAIN_RELAXED_POLL 1
+#endif
 
 namespace pg {
 
@@ -125,6 +128,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define STAMP(k) \
     if (P.dbg && threadIdx.x == 0) P.dbg[blockIdx.x * 16 + (k)] = gtimer()
 
+__device__ __forceinline__ unsigned long long xget(const unsigned long long* p);
 // Grid-wide barrier among consumer warps (the producer never blocks on it).
 // Monotone counter: generation g completes when the count reaches (g+1)*G.
 // The CTA barrier orders every consumer's z/act stores before thread 0's
@@ -137,8 +141,14 @@ __device__ __forceinline__ void grid_sync_consumers(unsigned long long* bar) {
         unsigned long long old;
         asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
         const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+#if CHAIN_RELAXED_POLL
+        while (xget(bar) < target) {
+        }
+        (void)ld_acquire(bar);
+#else
         while (ld_acquire(bar) < target) {
         }
+#endif
     }
     consumer_sync();
 }

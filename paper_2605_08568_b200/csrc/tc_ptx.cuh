@@ -20,6 +20,15 @@ __device__ __forceinline__ void u_mbar_wait(uint32_t b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ bool u_mbar_test(uint32_t b, uint32_t parity) {  // non-blocking phase test
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(b), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void u_mbar_arrive_tx(uint32_t b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
 }

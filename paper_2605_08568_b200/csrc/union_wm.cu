@@ -296,7 +296,6 @@ __global__ void __launch_bounds__(WM_THREADS, 1) k_union_wm(const __grid_constan
                 wm_bar_epi();
                 if (warp == 2 && lane == 0) {
                     WM_STAMP(9);
-                    __threadfence();
                     st_release(P.flags + pair * 2 + (int)rank, tag);
                     WM_STAMP(10);
                 }
@@ -324,8 +323,9 @@ __global__ void __launch_bounds__(WM_THREADS, 1) k_union_wm(const __grid_constan
                 const int pp = pp0 + lane;
                 if (pp < pf + n) {
                     const unsigned* f = P.flags + pp * 2 + (int)rank;
-                    while (ld_acquire(f) != tag) {
+                    while (ld_relaxed(f) != tag) {
                     }
+                    (void)ld_acquire(f);
                 }
             }
             __syncwarp();
