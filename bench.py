@@ -908,29 +908,47 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
                 pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
                 reduce(yd[nm])
 
+    def decode():  # decode alone (the HBM-bound part): 8 tokens through the 7 sharded linears
+        for _ in range(n_dec):
+            for nm, (agg, m, n, own) in lins.items():
+                pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
+                reduce(yd[nm])
+
     with torch.cuda.stream(st):
         for _ in range(3):
             step()
     st.synchronize()
+    # one CUDA graph per step (and per 8-token decode run): the per-linear launches
+    # are shorter than their Python dispatch; NCCL all-reduces are captured too
+    graphs = {}
+    try:
+        for key, fn in (("step", step), ("decode", decode)):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=st):
+                fn()
+            graphs[key] = gr
+    except Exception:  # noqa: BLE001 -- eager fallback, reported below
+        graphs = {}
+    run_step = graphs["step"].replay if graphs else step
+    run_dec = graphs["decode"].replay if graphs else decode
     barrier(torch, world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(st):
+        run_step()
         e0.record(st)
         for _ in range(reps):
-            step()
+            run_step()
         e1.record(st)
     st.synchronize()
     ms = max_over_ranks(torch, e0.elapsed_time(e1) / reps, dev, world)
-    # decode alone (the HBM-bound part): 8 tokens through the 7 sharded linears
     with torch.cuda.stream(st):
+        run_dec()
         e0.record(st)
         for _ in range(reps):
-            for nm, (agg, m, n, own) in lins.items():
-                pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
-                reduce(yd[nm])
+            run_dec()
         e1.record(st)
     st.synchronize()
-    us_dec = max_over_ranks(torch, e0.elapsed_time(e1) / reps * 1e3, dev, world)
+    us_dec = max_over_ranks(torch, e0.elapsed_time(e1) / reps / n_dec * 1e3, dev, world)
     hbm_peak, tensor_peak, peak_kind = peaks()
     dec_bytes = sum(own * (m + n) * 2 for (_, m, n, own) in lins.values())  # this rank's selected experts
     flops = 2 * T_pre * sum(ldims[nm][1] * (m + n) for nm, (m, n) in LIN13.items())
@@ -943,7 +961,7 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
             "decode_roofline": {"bound": "hbm", "alg_bytes_per_token_rank0": dec_bytes,
                                 "achieved": dec_bytes / (us_dec * 1e-6) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                                 "frac": dec_bytes / (us_dec * 1e-6) / 1e9 / hbm_peak, "peak_kind": peak_kind},
-            "prefill_flops_per_step": flops,
+            "prefill_flops_per_step": flops, "graph": bool(graphs),
             "collective": "torch.distributed.all_reduce (NCCL) of every linear's partial" if world > 1
             else "none (world 1: one shard holds every expert)"}
 
