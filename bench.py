@@ -898,21 +898,33 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
         if world > 1:
             torch.distributed.all_reduce(y)
 
+    act = torch.empty(13824, device=dev, dtype=torch.bfloat16)
+
+    def decode_token():
+        if world == 1:
+            # one shard holds every expert: q/k/v as one fused module launch, o, and
+            # the MLP block as one k_chain launch (up/gate -> silu -> down)
+            pg.module_forward([lins[nm][0] for nm in ("q", "k", "v")], 0, xd, out_dtype=torch.float32,
+                              outs=[yd[nm] for nm in ("q", "k", "v")])
+            pg.aggregated_forward(lins["o"][0], 0, xd, out_dtype=torch.float32, out=yd["o"])
+            pg.mlp_forward(lins["up"][0], lins["gate"][0], lins["down"][0], 0, xd, out_dtype=torch.float32,
+                           out=yd["down"], act=act)
+            return
+        for nm, (agg, m, n, own) in lins.items():  # sharded: every linear's partial all-reduced
+            pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
+            reduce(yd[nm])
+
     def step():
         for nm, (agg, m, n, own) in lins.items():  # prefill chunk: T=256 tokens through each linear
             x = xpf if n == 13824 else xp
             pg.aggregated_forward_batched(agg, [0], [0, T_pre], x, out_dtype=torch.float32, out=yp[nm])
             reduce(yp[nm])
         for _ in range(n_dec):  # decode tokens reusing S
-            for nm, (agg, m, n, own) in lins.items():
-                pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
-                reduce(yd[nm])
+            decode_token()
 
     def decode():  # decode alone (the HBM-bound part): 8 tokens through the 7 sharded linears
         for _ in range(n_dec):
-            for nm, (agg, m, n, own) in lins.items():
-                pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
-                reduce(yd[nm])
+            decode_token()
 
     with torch.cuda.stream(st):
         for _ in range(3):
@@ -962,6 +974,8 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
                                 "achieved": dec_bytes / (us_dec * 1e-6) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                                 "frac": dec_bytes / (us_dec * 1e-6) / 1e9 / hbm_peak, "peak_kind": peak_kind},
             "prefill_flops_per_step": flops, "graph": bool(graphs),
+            "decode_path": "world 1: q/k/v fused module + o + fused MLP block (k_chain), 3 launches per token"
+            if world == 1 else "per linear: aggregated_forward + NCCL all-reduce of the partial",
             "collective": "torch.distributed.all_reduce (NCCL) of every linear's partial" if world > 1
             else "none (world 1: one shard holds every expert)"}
 
