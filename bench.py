@@ -681,14 +681,18 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
 
     have_dev_pack = hasattr(pg, "pack_selected")
 
-    bufs = {}
+    bufs = {False: {}, True: {}}
+    have_gather = have_dev_pack and hasattr(pg, "PackedExperts") and hasattr(pg.PackedExperts, "gathered")
 
-    def pack_all():  # device pack into persistent buffers (no allocation inside the timed region)
+    def pack_all(gather=False):  # device pack into persistent buffers (no allocation inside the timed region)
+        # gather=True: A columns only; the stage-1 GEMM gathers the B^T rows (TMA gather4)
         if not have_dev_pack:
             return None
+        b = bufs[gather]
         for nm in LIN:
-            bufs[nm] = pg.pack_selected(layers[nm][0], sels[nm], into=bufs.get(nm))
-        return dict(bufs)
+            b[nm] = (pg.pack_selected(layers[nm][0], sels[nm], into=b.get(nm), gather=True) if gather
+                     else pg.pack_selected(layers[nm][0], sels[nm], into=b.get(nm)))
+        return dict(b)
 
     def gemms(packs):
         for nm in LIN:
@@ -710,8 +714,11 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
     pack_ms_host = (time.perf_counter() - t0) * 1e3
     gemms(packs)
     torch.cuda.synchronize()
+    if have_gather:
+        gemms(pack_all(True))
+        torch.cuda.synchronize()
     reps = 5
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     barrier(torch, world)
     e[0].record()
     for _ in range(reps):
@@ -723,6 +730,12 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
     for _ in range(reps):
         gemms(packs)
     e[3].record()
+    for _ in range(reps if have_gather else 0):
+        gpacks = pack_all(True)
+    e[4].record()
+    for _ in range(reps if have_gather else 0):
+        gemms(gpacks)
+    e[5].record()
     barrier(torch, world)
     # the same packed GEMMs through cuBLAS (torch.bmm over the 16 prompts: the
     # batched-GEMM analogue of the grouped launch), z rounded to bf16 between
@@ -759,6 +772,17 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
     route_ms = max_over_ranks(torch, e[0].elapsed_time(e[1]) / reps, dev, world)
     pack_ms = max_over_ranks(torch, e[1].elapsed_time(e[2]) / reps, dev, world) if have_dev_pack else pack_ms_host
     ms = max_over_ranks(torch, e[2].elapsed_time(e[3]) / reps, dev, world)
+    modes = {"packed": {"pack_ms": pack_ms, "gemm_ms": ms,
+                        "what": "pack B^T rows + A columns per prompt, GEMMs over the packed arenas"}}
+    if have_gather:
+        gpack_ms = max_over_ranks(torch, e[3].elapsed_time(e[4]) / reps, dev, world)
+        gms = max_over_ranks(torch, e[4].elapsed_time(e[5]) / reps, dev, world)
+        modes["gathered"] = {"pack_ms": gpack_ms, "gemm_ms": gms,
+                             "what": "pack A columns only; the stage-1 GEMM gathers the selected B^T rows with "
+                                     "TMA gather4 (bit-identical results)"}
+        if gpack_ms + gms < pack_ms + ms:  # report the faster pipeline
+            pack_ms, ms = gpack_ms, gms
+    mode = min(modes, key=lambda k: modes[k]["pack_ms"] + modes[k]["gemm_ms"])
     _, tflops_peak, peak_kind = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
     out = {"workload": "config3: LLaMA-7B decoder layer (q,k,v,o,gate,up,down) ratio 0.6, 16 prompts x 2048 tokens, "
@@ -766,7 +790,7 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
            "tokens_per_s": P * T / ((ms + route_ms + pack_ms) * 1e-3) * world,
            "gemm_tokens_per_s": P * T / (ms * 1e-3) * world,
            "ms_per_layer": ms, "route_ms": route_ms, "pack_ms": pack_ms,
-           "pack_on_device": have_dev_pack,
+           "pack_on_device": have_dev_pack, "mode": mode, "modes": modes,
            "baselines": {"packed_gemms_cublas": None if cub_ms is None else {
                "ms_per_layer": cub_ms, "tflops": flops / (cub_ms * 1e-3) / 1e12,
                "what": "the same packed per-prompt GEMMs through cuBLAS (torch.bmm over the 16 prompts, "

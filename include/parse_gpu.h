@@ -315,6 +315,13 @@ int pg_pack_selected(pg_layer layer, const int32_t* sel_dev, size_t k, size_t n_
 int pg_prefill_packed(pg_layer layer, const void* bt_packed, const void* a_packed, size_t k,
                       const int64_t* offsets_host, size_t n_prompts, const void* x_dev, void* y_dev,
                       pg_dtype y_dtype, pg_stream stream);
+/* pg_prefill_gathered: pg_prefill_packed without the packed B^T arena -- the
+ * stage-1 GEMM gathers each prompt's selected B^T rows sel_dev[p*k + j]
+ * straight from the layer (TMA gather4); a_packed from pg_pack_selected with
+ * bt_out = NULL (A columns only).  Every prompt needs 0 or >= 256 tokens.
+ * Results are bit-identical to pg_prefill_packed. */
+int pg_prefill_gathered(pg_layer layer, const int32_t* sel_dev, const void* a_packed, size_t k, const int64_t* offsets,
+                        size_t n_prompts, const void* x, void* y, pg_dtype y_dtype, pg_stream stream);
 
 /* K5 primitive: C[M, N] = A[M, K] . B[N, K]^T on the tcgen05 tensor cores
  * (bf16 operands, both K-major with 16-byte aligned rows, f32 accumulation;

@@ -102,6 +102,7 @@ _SIGS = {
     "pg_pack_bytes": [_vp, _sz, _sz, _sp, _sp],
     "pg_pack_selected": [_vp, _vp, _sz, _sz, _vp, _vp, _vp],
     "pg_prefill_packed": [_vp, _vp, _vp, _sz, _i64p, _sz, _vp, _vp, _i, _vp],
+    "pg_prefill_gathered": [_vp, _vp, _vp, _sz, _i64p, _sz, _vp, _vp, _i, _vp],
     "pg_mlp_forward": [_vp, _vp, _vp, _sp, _vp, _vp, _vp, _vp, _i, _vp],
     "pg_mlp_forward_chain": [_vp, _vp, _vp, _sp, _sz, _vp, _vp, _vp, _i, _vp],
 }

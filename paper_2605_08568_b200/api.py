@@ -725,15 +725,25 @@ class PackedExperts:
     exec_engine.hpp:112-164 with one pattern per prompt): B^T rows [P, kp, ldb]
     and A columns [P, m, kp] in caller-owned (torch) buffers."""
 
-    def __init__(self, layer: FactorizedLayer, k: int, n_prompts: int, bt: torch.Tensor, a: torch.Tensor):
+    def __init__(self, layer: FactorizedLayer, k: int, n_prompts: int, bt: torch.Tensor | None, a: torch.Tensor,
+                 sel: torch.Tensor | None = None):
         self.layer, self.k, self.P, self.bt, self.a = layer, k, n_prompts, bt, a
+        self.sel = sel  # gathered packs (bt is None): the selection the prefill gathers B^T rows by
+
+    @property
+    def gathered(self) -> bool:
+        return self.bt is None
 
 
-def pack_selected(layer: FactorizedLayer, sel: torch.Tensor, into: PackedExperts | None = None) -> PackedExperts:
+def pack_selected(layer: FactorizedLayer, sel: torch.Tensor, into: PackedExperts | None = None,
+                  gather: bool = False) -> PackedExperts:
     """Pack each prompt's selection sel [P, K] (device int32, ascending; the
     router's output) on the device -- no host round trip, no synchronisation.
     `into`: an earlier pack of the same layer and shape whose buffers are
-    reused (serving loops: no allocation per batch)."""
+    reused (serving loops: no allocation per batch).  gather=True packs the A
+    columns only: prefill_packed then gathers the selected B^T rows straight
+    from the layer inside the stage-1 GEMM (TMA gather4; `sel` must stay
+    unchanged until that prefill has run; prompts of 0 or >= 256 tokens)."""
     if not (isinstance(sel, torch.Tensor) and sel.is_cuda):
         raise ValueError("pack_selected: device selection tensor [P, K] expected")
     if sel.dim() == 1:
@@ -743,14 +753,15 @@ def pack_selected(layer: FactorizedLayer, sel: torch.Tensor, into: PackedExperts
     bb, ab = C.c_size_t(), C.c_size_t()
     call("pg_pack_bytes", layer.handle, k, P, C.byref(bb), C.byref(ab))
     if into is not None:
-        if into.layer is not layer or into.bt.numel() != bb.value or into.a.numel() != ab.value:
-            raise ValueError("pack_selected: `into` packs another layer / shape")
+        if (into.layer is not layer or into.gathered != gather or into.a.numel() != ab.value
+                or (not gather and into.bt.numel() != bb.value)):
+            raise ValueError("pack_selected: `into` packs another layer / shape / mode")
         bt, a = into.bt, into.a
     else:
-        bt = torch.empty(bb.value, dtype=torch.uint8, device=sel.device)
+        bt = None if gather else torch.empty(bb.value, dtype=torch.uint8, device=sel.device)
         a = torch.empty(ab.value, dtype=torch.uint8, device=sel.device)
-    call("pg_pack_selected", layer.handle, _ptr(sel), k, P, _ptr(bt), _ptr(a), _stream())
-    return PackedExperts(layer, k, P, bt, a)
+    call("pg_pack_selected", layer.handle, _ptr(sel), k, P, None if bt is None else _ptr(bt), _ptr(a), _stream())
+    return PackedExperts(layer, k, P, bt, a, sel if gather else None)
 
 
 def prefill_packed(packed: PackedExperts, offsets, x: torch.Tensor, out_dtype=None,
@@ -765,8 +776,12 @@ def prefill_packed(packed: PackedExperts, offsets, x: torch.Tensor, out_dtype=No
         raise ValueError("prefill_packed: bad X shape / offsets")
     ydt = _out_dtype(L.dtype, out_dtype)
     y = out if out is not None else torch.empty((x.shape[0], L.m), dtype=_TORCH[ydt], device=x.device)
-    call("pg_prefill_packed", L.handle, _ptr(packed.bt), _ptr(packed.a), packed.k,
-         offs.ctypes.data_as(C.POINTER(C.c_int64)), packed.P, _ptr(x), _ptr(y), ydt, _stream())
+    if packed.gathered:
+        call("pg_prefill_gathered", L.handle, _ptr(packed.sel), _ptr(packed.a), packed.k,
+             offs.ctypes.data_as(C.POINTER(C.c_int64)), packed.P, _ptr(x), _ptr(y), ydt, _stream())
+    else:
+        call("pg_prefill_packed", L.handle, _ptr(packed.bt), _ptr(packed.a), packed.k,
+             offs.ctypes.data_as(C.POINTER(C.c_int64)), packed.P, _ptr(x), _ptr(y), ydt, _stream())
     return y
 
 

@@ -1601,7 +1601,7 @@ extern "C" int pg_pack_bytes(pg_layer L, size_t k, size_t n_prompts, size_t* bt_
 extern "C" int pg_pack_selected(pg_layer L, const int32_t* sel_dev, size_t k, size_t P, void* bt_out, void* a_out,
                                 pg_stream s) {
     PG_API_BEGIN
-    require(L && sel_dev && bt_out && a_out && P > 0, PG_INVALID_ARGUMENT, "pack_selected: bad arguments");
+    require(L && sel_dev && a_out && P > 0, PG_INVALID_ARGUMENT, "pack_selected: bad arguments");
     require(L->dt == PG_BF16, PG_INVALID_ARGUMENT, "pack_selected: bf16 layers (tensor-core prefill path)");
     if (k == 0 || k > (size_t)L->r) throw Error{PG_INVALID_ARGUMENT, "select_topk: K out of range"};
     launch_pack_selected(L->bt, L->ldb, L->a, L->lda, L->r, L->n, L->m, sel_dev, (int)k, (int)P, bt_out, a_out,
@@ -1642,6 +1642,51 @@ extern "C" int pg_prefill_packed(pg_layer L, const void* bt_packed, const void* 
         void* zq = z.as<char>() + zo;
         zo += round_up((size_t)T * kp * 2, 256);
         s1.push_back(UmmaSpec{xq, L->n, bt, L->ldb, zq, kp, (int)T, kp, L->n, 1});
+        s2.push_back(UmmaSpec{zq, kp, a, kp, yq, L->m, (int)T, L->m, kp, ydt == PG_BF16 ? 1 : 0});
+    }
+    if (!s1.empty()) {
+        launch_umma(s1, st);
+        launch_umma(s2, st);
+    }
+    PG_API_END
+}
+
+extern "C" int pg_prefill_gathered(pg_layer L, const int32_t* sel_dev, const void* a_packed, size_t k,
+                                   const int64_t* offs, size_t P, const void* x, void* y, pg_dtype ydt, pg_stream s) {
+    PG_API_BEGIN
+    require(L && sel_dev && a_packed && offs && x && y && P > 0, PG_INVALID_ARGUMENT,
+            "prefill_gathered: bad arguments");
+    require(L->dt == PG_BF16 && L->n % 8 == 0, PG_INVALID_ARGUMENT, "prefill_gathered: bf16 layers, n % 8 == 0");
+    if (k == 0 || k > (size_t)L->r) throw Error{PG_INVALID_ARGUMENT, "select_topk: K out of range"};
+    check_ydt(L->dt, ydt);
+    const cudaStream_t st = as_stream(s);
+    const int kp = (int)round_up(k, 8);
+    const size_t ys = dtype_size(ydt);
+    size_t zbytes = 0;
+    for (size_t p = 0; p < P; ++p) {
+        const int64_t T = offs[p + 1] - offs[p];
+        require(T == 0 || T >= 256, PG_INVALID_ARGUMENT,
+                "prefill_gathered: every prompt needs 0 or >= 256 tokens (CTA-pair tiles); pack B^T for shorter ones");
+        zbytes += round_up((size_t)T * kp * 2, 256);
+    }
+    Scratch z(zbytes, st);
+    std::vector<UmmaSpec> s1, s2;
+    size_t zo = 0;
+    for (size_t p = 0; p < P; ++p) {
+        const int64_t t0 = offs[p], T = offs[p + 1] - offs[p];
+        if (T <= 0) continue;
+        const void* a = static_cast<const char*>(a_packed) + p * (size_t)L->m * kp * 2;
+        const void* xq = static_cast<const char*>(x) + t0 * L->n * 2;
+        void* yq = static_cast<char*>(y) + t0 * L->m * ys;
+        void* zq = z.as<char>() + zo;
+        zo += round_up((size_t)T * kp * 2, 256);
+        // stage 1: Z = X . B^T[sel]^T, the selected rows gathered by the GEMM's TMA
+        // (columns j >= k read zero rows -> zero Z padding for stage 2)
+        UmmaSpec a1{xq, L->n, L->bt, L->ldb, zq, kp, (int)T, kp, L->n, 1};
+        a1.b_idx = sel_dev + p * k;
+        a1.b_idx_n = (int)k;
+        a1.b_idx_rows = L->r;
+        s1.push_back(a1);
         s2.push_back(UmmaSpec{zq, kp, a, kp, yq, L->m, (int)T, L->m, kp, ydt == PG_BF16 ? 1 : 0});
     }
     if (!s1.empty()) {

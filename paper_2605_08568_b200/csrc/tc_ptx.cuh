@@ -118,6 +118,18 @@ __device__ __forceinline__ void u_tma_2d_pair_h(uint32_t dst, const CUtensorMap*
         : "memory");
 }
 
+// CTA pair, four gathered rows: rows r0..r3 of the map's tensor, columns
+// [x, x + box) each, land as four consecutive 128-byte rows at dst (the map's
+// swizzle applies as for a box load); out-of-range rows are zero-filled
+__device__ __forceinline__ void u_tma_gather4_pair_h(uint32_t dst, const CUtensorMap* map, int x, int r0, int r1, int r2,
+                                                     int r3, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;"
+        ::"r"(dst), "l"(map), "r"(x), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar), "l"(pol)
+        : "memory");
+}
+
 __device__ __forceinline__ void u_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"

@@ -37,6 +37,7 @@ constexpr int UM_SMEM = UM_STAGES * UM_STAGE_BYTES + 1024 /*align*/ + 256 /*barr
 
 constexpr int UM_MAX_GROUPS = 32;
 
+
 struct UmmaGroup {
     void* out;                 // [M, ldo] row-major
     long long ldo;
@@ -50,6 +51,8 @@ struct UmmaGroup {
     const int32_t* row_pat;
     int direct_epi;
     int a_hint, b_hint;
+    const int32_t* b_idx;  // gathered B rows (pair kernel), see UmmaSpec
+    int b_idx_n, b_idx_rows;
 };
 
 // Passed as one __grid_constant__ parameter block (< 32 KB): TMA reads the
@@ -61,6 +64,7 @@ struct __align__(64) UmmaParams {
     int ngroups;
     int total_tiles;
     int epi_deep;  // bf16 TMA-store epilogue: 4 x 2 KB staging slots per warp in flight (else 2)
+    int gather;    // some group gathers its B rows: the pair kernel's producer runs as a whole warp
 };
 
 // ---- epilogue helpers: TMEM -> registers -> bf16 / f32 -> global, with the
@@ -376,6 +380,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const UmmaGroup& G, const CUte
     }
 }
 
+// GATHER: some group gathers its B rows (one gather4 per producer lane); a
+// separate instantiation, so plain launches keep the lane-0 producer loop
+template <bool GATHER>
 __global__ void __launch_bounds__(P2_THREADS, 1) k_umma_grouped2(const __grid_constant__ UmmaParams P) {
     extern __shared__ __align__(1024) unsigned char usmem[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(usmem) + 1023) & ~uintptr_t(1023));
@@ -413,37 +420,59 @@ __global__ void __launch_bounds__(P2_THREADS, 1) k_umma_grouped2(const __grid_co
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
-        if (lane == 0) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            uint64_t pf, pl;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
-            int s = 0;
-            uint32_t ph = 0;
-            for (int t = pair; t < P.total_tiles; t += npairs) {
-                int g = 0;
-                while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
-                const UmmaGroup& G = P.groups[g];
-                const int lt = t - G.tile_base;
-                const int m0 = (lt % G.tiles_m) * 2 * UM_BM + (int)rank * UM_BM;
-                const int n0 = (lt / G.tiles_m) * G.bn + (int)rank * (G.bn / 2);
-                const int kbs = (G.K + UM_BK - 1) / UM_BK;
-                const uint32_t bytes = 2 * (UM_A_BYTES + (uint32_t)(G.bn / 2) * UM_BK * 2);  // both CTAs
-                for (int kb = 0; kb < kbs; ++kb) {
-                    u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
-                    const uint32_t fb = leader_addr(u_smem(&full[s]));
+        // lane 0 drives the ring; with gathered B rows every lane issues one
+        // gather4 (four rows) of this CTA's bn/2 rows per k-block (the whole-warp
+        // loop costs ~2.5 % on plain launches, so only gathering launches run it)
+        if (GATHER || lane == 0) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        uint64_t pf, pl, pn;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pn));
+        int s = 0;
+        uint32_t ph = 0;
+        for (int t = pair; t < P.total_tiles; t += npairs) {
+            int g = 0;
+            while (g + 1 < P.ngroups && P.groups[g + 1].tile_base <= t) ++g;
+            const UmmaGroup& G = P.groups[g];
+            const int lt = t - G.tile_base;
+            const int m0 = (lt % G.tiles_m) * 2 * UM_BM + (int)rank * UM_BM;
+            const int n0 = (lt / G.tiles_m) * G.bn + (int)rank * (G.bn / 2);
+            const int kbs = (G.K + UM_BK - 1) / UM_BK;
+            const uint32_t bytes = 2 * (UM_A_BYTES + (uint32_t)(G.bn / 2) * UM_BK * 2);  // both CTAs
+            const bool gat = GATHER && G.b_idx != nullptr, mine = gat && 4 * lane < G.bn / 2;
+            int gr0 = 0, gr1 = 0, gr2 = 0, gr3 = 0;
+            if (mine) {
+                const int j = n0 + 4 * lane;
+                gr0 = j < G.b_idx_n ? __ldg(G.b_idx + j) : G.b_idx_rows;
+                gr1 = j + 1 < G.b_idx_n ? __ldg(G.b_idx + j + 1) : G.b_idx_rows;
+                gr2 = j + 2 < G.b_idx_n ? __ldg(G.b_idx + j + 2) : G.b_idx_rows;
+                gr3 = j + 3 < G.b_idx_n ? __ldg(G.b_idx + j + 3) : G.b_idx_rows;
+            }
+            const uint64_t bpol = G.b_hint ? u_policy(G.b_hint, pf, pl) : pn;
+            for (int kb = 0; kb < kbs; ++kb) {
+                if (lane == 0) u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
+                if (GATHER) __syncwarp();
+                const uint32_t fb = leader_addr(u_smem(&full[s]));
+                unsigned char* st = base + s * U2_STAGE_BYTES;
+                if (lane == 0) {
                     if (leader) u_mbar_arrive_tx_cluster(fb, bytes);
-                    unsigned char* st = base + s * U2_STAGE_BYTES;
                     if (G.a_hint)
                         u_tma_2d_pair_h(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb, u_policy(G.a_hint, pf, pl));
                     else u_tma_2d_pair(u_smem(st), &P.maps[2 * g], kb * UM_BK, m0, fb);
-                    if (G.b_hint)
-                        u_tma_2d_pair_h(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb,
-                                        u_policy(G.b_hint, pf, pl));
-                    else u_tma_2d_pair(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
-                    if (++s == P2_STAGES) { s = 0; ph ^= 1; }
+                    if (!gat) {
+                        if (G.b_hint)
+                            u_tma_2d_pair_h(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb,
+                                            u_policy(G.b_hint, pf, pl));
+                        else u_tma_2d_pair(u_smem(st + U2_A_BYTES), &P.maps[2 * g + 1], kb * UM_BK, n0, fb);
+                    }
                 }
+                if (mine)
+                    u_tma_gather4_pair_h(u_smem(st + U2_A_BYTES) + (uint32_t)lane * 4 * UM_BK * 2, &P.maps[2 * g + 1],
+                                         kb * UM_BK, gr0, gr1, gr2, gr3, fb, bpol);
+                if (++s == P2_STAGES) { s = 0; ph ^= 1; }
             }
+        }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA)
@@ -725,7 +754,8 @@ static int umma_pairs_enabled() {
 void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
     once_per_device(reinterpret_cast<const void*>(&k_umma_grouped), [] {
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
-        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+        PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeMaxDynamicSharedMemorySize, U2_SMEM));
         PG_CUDA_THROW(cudaFuncSetAttribute(k_umma_grouped4, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     });
@@ -782,8 +812,18 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             if (s.bn > 0) G.bn = s.bn;
             else if (common_bn > 0) G.bn = std::min(G.bn, common_bn);
             P->maps[2 * g] = make_map(s.a, s.M, s.K, s.lda, UM_BM);
-            P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
-                                          mc ? G.bn / 4 : (pairs ? G.bn / 2 : G.bn));
+            if (s.b_idx) {  // gathered B rows: one-row boxes, four rows per TMA gather4
+                if (!pairs || mc)
+                    throw Error{PG_INVALID_ARGUMENT, "umma: gathered B rows need the CTA-pair kernel (M >= 256)"};
+                P->maps[2 * g + 1] = make_map(s.b, s.b_idx_rows, s.K, s.ldb, 1);
+            } else {
+                P->maps[2 * g + 1] = make_map(s.b, s.b_rows > 0 ? std::min(s.b_rows, s.N) : s.N, s.K, s.ldb,
+                                              mc ? G.bn / 4 : (pairs ? G.bn / 2 : G.bn));
+            }
+            G.b_idx = s.b_idx;
+            if (s.b_idx) P->gather = 1;
+            G.b_idx_n = s.b_idx_n;
+            G.b_idx_rows = s.b_idx_rows;
             static const int hints_env = [] {
                 const char* e = getenv("PG_UMMA_L2HINT");
                 return e ? atoi(e) : 1;
@@ -864,7 +904,7 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
                 q.attrs = a;
                 q.numAttrs = 1;
                 int n = 0;
-                if (cudaOccupancyMaxActiveClusters(&n, k_umma_grouped2, &q) != cudaSuccess || n <= 0) n = sms / 2;
+                if (cudaOccupancyMaxActiveClusters(&n, k_umma_grouped2<false>, &q) != cudaSuccess || n <= 0) n = sms / 2;
                 if (getenv("PG_UMMA_DEBUG")) fprintf(stderr, "umma2: max active clusters %d (sms %d)\n", n, sms);
                 return n;
             }();
@@ -882,7 +922,8 @@ void launch_umma(const std::vector<UmmaSpec>& specs, cudaStream_t st) {
             at[1].val.programmaticStreamSerializationAllowed = umma_pdl();
             cfg.attrs = at;
             cfg.numAttrs = 2;
-            PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped2, *P));
+            if (P->gather) PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped2<true>, *P));
+            else PG_CUDA_THROW(cudaLaunchKernelEx(&cfg, k_umma_grouped2<false>, *P));
             count_launch();
         } else {
             cudaLaunchConfig_t cfg = {};

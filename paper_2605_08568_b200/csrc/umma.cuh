@@ -29,6 +29,11 @@ struct UmmaSpec {
     int bn = 0;      // tile width override (0: chosen by launch_umma)
     int a_hint = 0, b_hint = 0;  // L2 policy of the operand loads: 0 default, 1 evict-first, 2 evict-last
     int direct_epi = 0;  // CTA-pair kernel: store from registers instead of the TMA-store epilogue
+    // optional gathered B rows (CTA-pair kernel): row j of the B operand is row
+    // b_idx[j] of `b` for j < b_idx_n, zero for j >= b_idx_n (TMA gather4 straight
+    // from the unpacked arena; b_idx_rows = rows of `b` in memory)
+    const int32_t* b_idx = nullptr;
+    int b_idx_n = 0, b_idx_rows = 0;
 };
 
 // C = A . B^T with K split across CTAs when the M x N tiles cannot cover the

@@ -166,9 +166,11 @@ void launch_pack_selected(const void* bt, int64_t ldb, const void* a, int64_t ld
                           const int32_t* sel, int k, int P, void* bt_out, void* a_out, cudaStream_t st) {
     const int kp = (k + 7) / 8 * 8;
     if (P <= 0 || k <= 0) return;
-    k_pack_rows_batched<<<dim3(kp, P), 128, 0, st>>>(static_cast<const int4*>(bt), ldb / 8, sel, k, kp,
-                                                     (n + 7) / 8, static_cast<int4*>(bt_out), ldb / 8);
-    PG_LAUNCH_CHECK();
+    if (bt_out) {  // (null: the prefill gathers the B^T rows itself, pg_prefill_gathered)
+        k_pack_rows_batched<<<dim3(kp, P), 128, 0, st>>>(static_cast<const int4*>(bt), ldb / 8, sel, k, kp,
+                                                         (n + 7) / 8, static_cast<int4*>(bt_out), ldb / 8);
+        PG_LAUNCH_CHECK();
+    }
     const size_t smem = (size_t)kPackRows * ((r + 7) / 8 * 8) * 2 + (size_t)kp * 4;
     if (smem > 48 * 1024)
         PG_CUDA_THROW(cudaFuncSetAttribute(k_pack_cols_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

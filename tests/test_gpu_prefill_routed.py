@@ -71,6 +71,11 @@ def test_routed_prefill_config3(pg, port, m, n):
     pk = pg.pack_selected(L, sel)
     y2 = pg.prefill_packed(pk, offs, X, out_dtype=torch.float32)
     assert torch.equal(pg.prefill_packed(pg.pack_selected(L, sel), offs, X, out_dtype=torch.float32), y2)
+    # the B^T rows gathered inside the stage-1 GEMM (TMA gather4, A packed only):
+    # the same operands in the same order -> bit-identical to the packed path
+    pkg = pg.pack_selected(L, sel, gather=True)
+    assert pkg.gathered and pkg.bt is None
+    assert torch.equal(pg.prefill_packed(pkg, offs, X, out_dtype=torch.float32), y2)
 
     # reference of the kernel's math: z = bf16(x B_S) accumulated in f64 (an
     # fp32-accumulated torch reference is itself ~2e-3 off at K = 11008 over
@@ -123,3 +128,41 @@ def test_pack_selected_layout(pg, port):
         assert not bt[p, K:].any()
     with pytest.raises(ValueError):
         pg.pack_selected(L, sels)  # host array: the device path only
+
+
+@pytest.mark.parametrize("K", [93, 96, 200])
+def test_prefill_gathered_ragged(pg, K):
+    """Gathered B^T rows (pg_prefill_gathered) vs the packed arena on ragged
+    prompts (0, 256, 300, 517 tokens), K not a multiple of 8 or 4 (padding rows
+    read as zero through out-of-range gather coordinates), a reused `into`
+    buffer, bf16 and f32 outputs: bit-identical."""
+    m, n, r = 384, 512, 240
+    rng = np.random.default_rng(K)
+    A = rng.standard_normal((m, r)) / np.sqrt(m)
+    B = rng.standard_normal((n, r)) / np.sqrt(n)
+    L = pg.FactorizedLayer(A, B, K, dtype="bf16")
+    lens = [256, 0, 300, 517]
+    offs = np.concatenate([[0], np.cumsum(lens)]).tolist()
+    Pp = len(lens)
+    sels = np.stack([np.sort(rng.choice(r, K, replace=False)) for _ in range(Pp)]).astype(np.int32)
+    sel = torch.from_numpy(sels).cuda()
+    g = torch.Generator(device="cuda").manual_seed(K)
+    X = torch.randn(offs[-1], n, device="cuda", generator=g).to(torch.bfloat16)
+    pk = pg.pack_selected(L, sel)
+    pkg = pg.pack_selected(L, sel, gather=True)
+    for dt in (torch.float32, torch.bfloat16):
+        y_pack = pg.prefill_packed(pk, offs, X, out_dtype=dt)
+        y_gath = pg.prefill_packed(pkg, offs, X, out_dtype=dt)
+        assert torch.equal(y_gath, y_pack)
+    # reuse of the gathered buffers with another selection
+    sels2 = np.stack([np.sort(rng.choice(r, K, replace=False)) for _ in range(Pp)]).astype(np.int32)
+    sel2 = torch.from_numpy(sels2).cuda()
+    pkg2 = pg.pack_selected(L, sel2, into=pkg, gather=True)
+    assert pkg2.a.data_ptr() == pkg.a.data_ptr()
+    y2 = pg.prefill_packed(pkg2, offs, X, out_dtype=torch.float32)
+    assert torch.equal(y2, pg.prefill_packed(pg.pack_selected(L, sel2), offs, X, out_dtype=torch.float32))
+    with pytest.raises(ValueError):
+        pg.pack_selected(L, sel2, into=pk, gather=True)  # mode mismatch
+    # prompts shorter than a CTA-pair tile are refused by the gathered path
+    with pytest.raises(Exception):
+        pg.prefill_packed(pkg, [0, 100, 356, 656, 1073], torch.zeros(1073, n, device="cuda", dtype=torch.bfloat16))

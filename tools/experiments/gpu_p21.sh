@@ -1,0 +1,1 @@
+for v in "" wp0 "" wp0; do PG_LIB_VARIANT=$v timeout 200 python tools/experiments/exp_prefill.py 2>&1 | grep "prefill P" | sed "s/^/v=$v /"; done
