@@ -94,6 +94,81 @@ __global__ void __launch_bounds__(128) k_mean_pool_tm_bf16x2(const __nv_bfloat16
     h[(int64_t)p * n + 2 * i2 + 1] = __ddiv_rn(s1, T);
 }
 
+// bf16, n % V == 0 (V = 4 or 8): V features per thread (one 8- or 16-byte
+// load per token: a warp reads 256 / 512 contiguous bytes of each token row
+// instead of 128), V strictly ordered fp64 chains per thread (the reference's
+// token order per feature); B tokens per batch, double buffered
+template <int V>
+struct PoolVec;
+template <>
+struct PoolVec<4> {
+    using T = uint2;
+    __device__ static void words(const uint2& v, uint32_t (&w)[2]) { w[0] = v.x; w[1] = v.y; }
+};
+template <>
+struct PoolVec<8> {
+    using T = uint4;
+    __device__ static void words(const uint4& v, uint32_t (&w)[4]) { w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; }
+};
+template <int V>
+__device__ __forceinline__ void poolv_add1(const typename PoolVec<V>::T& v, double (&s)[V]) {
+    uint32_t w[V / 2];
+    PoolVec<V>::words(v, w);
+#pragma unroll
+    for (int e = 0; e < V / 2; ++e) {
+        s[2 * e] = __dadd_rn(s[2 * e], (double)__uint_as_float(w[e] << 16));
+        s[2 * e + 1] = __dadd_rn(s[2 * e + 1], (double)__uint_as_float(w[e] & 0xffff0000u));
+    }
+}
+template <int V, int B>
+__global__ void __launch_bounds__(64) k_mean_pool_tm_bf16v(const __nv_bfloat16* __restrict__ x, int n,
+                                                          const int64_t* __restrict__ offs, double* __restrict__ h) {
+    using LT = typename PoolVec<V>::T;
+    const int p = blockIdx.y;
+    const int iv = blockIdx.x * blockDim.x + threadIdx.x;  // feature group
+    if (V * iv >= n) return;
+    const int64_t t0 = offs[p], t1 = offs[p + 1];
+    const LT* col = reinterpret_cast<const LT*>(x) + iv;
+    const int64_t ld = n / V;
+    double s[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) s[e] = 0.0;
+    const int64_t nb = (t1 - t0) / B;  // whole batches
+    LT va[B], vb[B];
+    auto load = [&](LT (&v)[B], int64_t t) {
+#pragma unroll
+        for (int u = 0; u < B; ++u) v[u] = __ldg(col + (t + u) * ld);
+    };
+    auto add = [&](const LT (&v)[B]) {
+#pragma unroll
+        for (int u = 0; u < B; ++u) poolv_add1<V>(v[u], s);
+    };
+    if (nb > 0) load(va, t0);
+    for (int64_t b = 0; b < nb; b += 2) {
+        if (b + 1 < nb) load(vb, t0 + (b + 1) * B);
+        add(va);
+        if (b + 1 >= nb) break;
+        if (b + 2 < nb) load(va, t0 + (b + 2) * B);
+        add(vb);
+    }
+    for (int64_t t = t0 + nb * B; t < t1; ++t) poolv_add1<V>(__ldg(col + t * ld), s);
+    const double T = (double)(t1 - t0);
+#pragma unroll
+    for (int e = 0; e < V; ++e) h[(int64_t)p * n + V * iv + e] = __ddiv_rn(s[e], T);
+}
+#ifndef POOL_V
+#define POOL_V 4
+#endif
+#ifndef POOL_B
+#define POOL_B 16
+#endif
+#ifndef POOL_MIN_N
+#define POOL_MIN_N 8192  // narrower rows keep the two-feature kernel (more warps in flight wins there)
+#endif
+#ifndef POOL_BLOCK
+#define POOL_BLOCK 64
+#endif
+
 // feature-major x [n, Ttot]: each warp owns 32 rows; a 32x32 tile is read
 // coalesced along tokens, then each lane sums its own row in token order.
 template <typename TX>
@@ -469,7 +544,16 @@ k_route_select(const double* __restrict__ zfast, const double* __restrict__ bnd,
 template <typename TX>
 static void launch_mean_pool_t(const void* x, pg_layout lay, int n, int64_t ttot,
                                const int64_t* offs_dev, int P, double* h, cudaStream_t st) {
-    if (lay == PG_TOKEN_MAJOR && sizeof(TX) == 2 && n % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0) {
+    static const int poolv = [] {  // 0: two features per thread (round-1 kernel)
+        const char* e = getenv("PG_POOLV");
+        return e ? atoi(e) : 1;
+    }();
+    if (poolv && n >= POOL_MIN_N && lay == PG_TOKEN_MAJOR && sizeof(TX) == 2 && n % POOL_V == 0 &&
+        reinterpret_cast<uintptr_t>(x) % (2 * POOL_V) == 0) {
+        dim3 g((n / POOL_V + POOL_BLOCK - 1) / POOL_BLOCK, P);
+        k_mean_pool_tm_bf16v<POOL_V, POOL_B><<<g, POOL_BLOCK, 0, st>>>(static_cast<const __nv_bfloat16*>(x), n,
+                                                                       offs_dev, h);
+    } else if (lay == PG_TOKEN_MAJOR && sizeof(TX) == 2 && n % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0) {
         dim3 g((n / 2 + 127) / 128, P);
         k_mean_pool_tm_bf16x2<<<g, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(x), n, offs_dev, h);
     } else if (lay == PG_TOKEN_MAJOR) {

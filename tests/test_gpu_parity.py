@@ -148,10 +148,12 @@ def test_route_select_pooled_matches_reference(pg, port):
             assert np.array_equal(got[p].astype(np.uint32), want), (seed, p)
 
 
-def test_mean_pool_bf16_token_major_batched(pg, port):
-    """bf16 token-major pooling (two features per thread, 64 tokens in flight)
-    is the reference's sequential fp64 sum on the bf16 values, bit for bit."""
-    n = 1030
+@pytest.mark.parametrize("n", [1030, 8196])
+def test_mean_pool_bf16_token_major_batched(pg, port, n):
+    """bf16 token-major pooling (n < 8192: two features per thread, 64 tokens
+    in flight; n >= 8192: four features per thread, 16-token batches) is the
+    reference's sequential fp64 sum on the bf16 values, bit for bit -- ragged
+    prompts around the batch sizes, a tail shorter than a batch."""
     lens = [1, 63, 64, 65, 129, 200, 3]
     offs = np.concatenate([[0], np.cumsum(lens)])
     X = port.gaussian(95, (offs[-1], n))
@@ -162,11 +164,11 @@ def test_mean_pool_bf16_token_major_batched(pg, port):
         assert np.array_equal(h[p], port.mean_pool(Xr[offs[p]:offs[p + 1]].T)), p
 
 
-def test_mean_pool_long_prompts_adversarial_columns(pg, port):
+@pytest.mark.parametrize("n", [512, 8192])
+def test_mean_pool_long_prompts_adversarial_columns(pg, port, n):
     """Long prompts with adversarial columns (tiny and huge values in one
     feature, a bf16-subnormal-range value, Inf, exact cancellation) pool to the
-    reference's sequential sum bit for bit."""
-    n = 512
+    reference's sequential sum bit for bit (both token-major bf16 kernels)."""
     lens = [2048, 1500, 777]
     offs = np.concatenate([[0], np.cumsum(lens)])
     X = port.gaussian(96, (offs[-1], n))
