@@ -674,10 +674,35 @@ def config3_arm(args, rank, world, local_rank, P=16, T=2048):
     src = {"q": X, "k": X, "v": X, "up": X, "gate": X, "o": Xo, "down": X2}
     sels = {}
 
+    # the seven routers are independent given their pooled inputs: four side
+    # streams forked from / joined to the current one (pool X -> q, k, v | up,
+    # gate; pool Xo -> o; pool X2 -> down), so the narrow score / select
+    # launches of one router fill the SMs another leaves idle
+    side = [torch.cuda.Stream(device=dev) for _ in range(4)]
+    lanes = [(X, ("q", "k", "v")), (None, ("up", "gate")), (Xo, ("o",)), (X2, ("down",))]
+
     def route_all():
-        pooled = {id(x): pg.mean_pool(x, layout="token", offsets=offs) for x in (X, Xo, X2)}
-        for nm in LIN:
-            sels[nm] = pg.route_select_pooled(routers[nm], pooled[id(src[nm])], layers[nm][1])
+        cur = torch.cuda.current_stream(dev)
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        pooled_x = torch.cuda.Event()
+        hx = None
+        for i, (inp, names) in enumerate(lanes):
+            st_i = side[i]
+            st_i.wait_event(fork)
+            with torch.cuda.stream(st_i):
+                if inp is None:  # up / gate reuse X's pooling
+                    st_i.wait_event(pooled_x)
+                    h = hx
+                else:
+                    h = pg.mean_pool(inp, layout="token", offsets=offs)
+                    if inp is X:
+                        hx = h
+                        pooled_x.record(st_i)
+                for nm in names:
+                    sels[nm] = pg.route_select_pooled(routers[nm], h, layers[nm][1])
+        for st_i in side:
+            cur.wait_stream(st_i)
 
     have_dev_pack = hasattr(pg, "pack_selected")
 
