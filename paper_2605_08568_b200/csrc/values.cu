@@ -120,7 +120,10 @@ __global__ void k_pack_rows_batched(const int4* __restrict__ src, int64_t lds16,
     for (int v = threadIdx.x; v < nv; v += blockDim.x) d[v] = ld_stream(s + v);
 }
 
-constexpr int kPackRows = 8;  // A rows staged per CTA (amortises each prompt's selection list)
+#ifndef PACK_ROWS
+#define PACK_ROWS 8
+#endif
+constexpr int kPackRows = PACK_ROWS;  // A rows staged per CTA (amortises each prompt's selection list)
 // (measured: staging every prompt's ids at once instead of one prompt at a
 // time was slower -- the random 2-byte shared-memory gathers bound the kernel)
 __global__ void __launch_bounds__(256) k_pack_cols_batched(const uint16_t* __restrict__ src, int64_t lds, int r,
