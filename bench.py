@@ -983,7 +983,8 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
     # are shorter than their Python dispatch; NCCL all-reduces are captured too
     graphs = {}
     try:
-        for key, fn in (("step", step), ("decode", decode)):
+        # world > 1: eager (NCCL all-reduces are not captured; no multi-GPU box to validate that here)
+        for key, fn in ((("step", step), ("decode", decode)) if world == 1 else ()):
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=st):
                 fn()
