@@ -69,9 +69,6 @@ constexpr int UP_MAXG = 4;
 #endif
 constexpr int UP_POLL_NS = UP_POLL_NS_CFG;  // back-off between polls of a dependency counter
 constexpr int UP_CSTRIDE = 32;   // ready counters one per 128-byte line
-#ifndef UP_WPF
-#define UP_WPF 0  // W tiles prefetched into L2 beyond the ring while it is full (k-blocks; 0 = off)
-#endif
 #ifndef UP_DRAIN_DIRECT
 #define UP_DRAIN_DIRECT 0
 #endif
@@ -272,36 +269,13 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
             asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pnorm));
             int s = 0, issued = 0, lastf = -1;
             uint32_t ph = 0;
-#if UP_WPF
-            // L2 prefetch cursor: while the ring is full (the consumers sit in a
-            // phase tail), pull the W tiles after the ring's into L2, at most
-            // UP_WPF k-blocks ahead of the issue cursor
-            int pr = r0, pkb = r0 < r1 ? P.recs[r0].k0 : 0, pcount = 0;
-            auto pf_step = [&]() {
-                if (pr >= r1) return;
-                const UpRec& Q = P.recs[pr];
-                if (pcount >= issued + UP_STAGES)
-                    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&P.groups[Q.g].wmap),
-                                 "r"(pkb * WM_BK), "r"(Q.row0 + (int)rank * WM_BM)
-                                 : "memory");
-                ++pcount;
-                if (++pkb >= Q.k1 && ++pr < r1) pkb = P.recs[pr].k0;
-            };
-#endif
             for (int i = r0; i < r1; ++i) {
                 const UpRec& R = P.recs[i];
                 if (i + 1 < r1) prefetch_l1(&P.recs[i + 1]);
                 const CUtensorMap* wm = &P.groups[R.g].wmap;
                 const int row = R.row0 + (int)rank * WM_BM, k1 = R.k1, f = R.phase;
                 for (int kb = R.k0; kb < k1; ++kb, ++issued) {
-#if UP_WPF
-                    while (pcount < issued + UP_STAGES && pr < r1) pf_step();  // catch up (no prefetch inside the ring)
-                    if (issued >= UP_STAGES)
-                        while (!u_mbar_test(u_smem(&empty[s]), ph ^ 1))
-                            if (pcount < issued + UP_STAGES + UP_WPF) pf_step();
-#else
                     if (issued >= UP_STAGES) u_mbar_wait(u_smem(&empty[s]), ph ^ 1);
-#endif
                     const uint32_t fb = leader_addr(u_smem(&full[s]));
                     if (leader) u_mbar_arrive_tx_cluster(fb, 2u * WM_W_BYTES);
                     u_tma_2d_pair_h(u_smem(base + s * UP_STAGE_BYTES), wm, kb * WM_BK, row, fb, R.w_hint ? pfirst : pnorm);
