@@ -64,7 +64,16 @@ k_cosine_scan(const double* __restrict__ emb, const double* __restrict__ q, int 
 // each lane keeping 8 double2 loads in flight (the one-warp-per-entry scan
 // leaves ~4 KB in flight per warp: latency-bound at N = 1024).  Partial sums
 // meet in shared memory; the bound argument is order-independent.
-constexpr int kCosWPE = 4, kCosEPB = 2;
+#ifndef COS_WPE
+#define COS_WPE 4
+#endif
+#ifndef COS_EPB
+#define COS_EPB 8  // entries per block: 1024 threads, the query staged once per 8 entries
+#endif
+#ifndef COS_BPS
+#define COS_BPS 2  // blocks per SM at most (each stages the query once)
+#endif
+constexpr int kCosWPE = COS_WPE, kCosEPB = COS_EPB;
 __global__ void __launch_bounds__(kCosWPE * kCosEPB * 32)
 k_cosine_scan_wide(const double* __restrict__ emb, const double* __restrict__ q, int N, int d,
                    double* __restrict__ sim, double* __restrict__ bnd) {
@@ -290,7 +299,7 @@ void launch_cosine_scan(const double* emb, const double* q, int N, int d, double
         return e ? atoi(e) : 1;
     }();
     if (wide_env && d % 8 == 0) {
-        const int blocks = min((N + kCosEPB - 1) / kCosEPB, kNumSMs * 8);
+        const int blocks = min((N + kCosEPB - 1) / kCosEPB, kNumSMs * COS_BPS);
         k_cosine_scan_wide<<<blocks, kCosWPE * kCosEPB * 32, (size_t)d * 8 + kCosEPB * kCosWPE * 32, st>>>(
             emb, q, N, d, sim, bnd);
         PG_LAUNCH_CHECK();
