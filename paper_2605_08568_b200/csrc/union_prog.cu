@@ -121,7 +121,8 @@ struct UpParams {
     float* partial;            // [2][pairs][2][WM_PART_FLOATS]
     unsigned long long* epoch;
     unsigned long long* dbg;
-    int exp;  // PG_PROG_EXP (timing experiments only, wrong results): 1 no reduction loads, 2 no partial drain, 4 no whole-tile stores
+    int exp;  // PG_PROG_EXP (timing experiments only, wrong results): 1 no reduction loads, 2 no partial drain,
+              // 4 no whole-tile stores, 8 half the tokens drained and reduced
 };
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 wm_epi_direct(P.Tp, P.T, G, taddr, R.row0 + (int)rank * WM_BM + q * 32, tps + R.tok_off, stg, lane, h,
                               UP_EPI_H);
             } else {
-                up_epi_partial_bulk(P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
+                up_epi_partial_bulk((P.exp & 8) ? P.Tp / 2 : P.Tp, taddr, P.partial + ((size_t)(set * np + pair) * 2 + rank) * WM_PART_FLOATS, q,
                                     h, reinterpret_cast<float*>(stage), lane, et);
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_union_prog(const __grid_const
                 const int row0 = S.row0 + (int)rank * WM_BM;
                 // token slice of this participant, 4-aligned (float4 along tokens)
                 const int ta = me * (P.Tp / 4) / n * 4, tb = min(P.T, (me + 1) * (P.Tp / 4) / n * 4);
-                const int cnt = max(0, tb - ta);
+                const int cnt = (P.exp & 8) ? max(0, tb - ta) / 2 : max(0, tb - ta);  // (exp 8: half the tail bytes, timing only)
                 // the slice's mask bytes (stage-1 outputs) into the idle staging
                 // buffer while the participants finish: [cnt tokens][128 rows]
                 uint8_t* const msk = stage;
