@@ -88,7 +88,7 @@ def module_ref(lay, nm, xin, pid):
 
 
 @pytest.mark.parametrize("D,F,T,layers,P", [(512, 1024, 96, 3, 12), (512, 1024, 256, 2, 40),
-                                            (1024, 2816, 5, 2, 3)])
+                                            (1024, 2816, 5, 2, 3), (512, 1024, 1, 1, 1), (512, 1024, 33, 2, 7)])
 def test_union_program_small(pg, D, F, T, layers, P):
     dims = {nm: (300, 150) for nm in ("q", "k", "v", "o")}
     dims.update({"up": (700, 350), "gate": (700, 350), "down": (640, 320)})
