@@ -703,3 +703,43 @@ def test_mlp_forward_chain_matches_blockwise(pg, port, nblocks, d, ff):
     g = port.masked_forward(*rd["gate"], pats[pids[0][1]][1], xr)
     ref = port.masked_forward(*rd["down"], pats[pids[0][2]][2], bf16_round(_silu(g) * u))
     assert rel(ys[0].double().cpu().numpy()[:, None], ref) <= 4e-3
+
+
+def test_13b_decode_block_fused_paths(pg):
+    """The config-5 decode token as the bench times it at world 1 (LLaMA-13B
+    shapes, ratio 0.4): q/k/v as one fused module launch, and the MLP block
+    (up/gate -> silu -> down) as one k_chain launch, vs an f64 reference of
+    rank_experts.hpp:52-72 on the same bf16 weights and selections (act rounded
+    to bf16 between the phases, as the kernel does)."""
+    dev = torch.device("cuda")
+    shapes = {"q": (5120, 5120), "k": (5120, 5120), "v": (5120, 5120),
+              "up": (13824, 5120), "gate": (13824, 5120), "down": (5120, 13824)}
+    dims = {nm: (pg.store_rank(pg.single_layer_k(m, n, 0.4), n), pg.single_layer_k(m, n, 0.4))
+            for nm, (m, n) in shapes.items()}
+    pats = pg.make_patterns(5151, 1, [dims[nm] for nm in shapes])[0]
+    g = torch.Generator(device=dev).manual_seed(13)
+    W, aggs, sel = {}, {}, {}
+    for j, (nm, (m, n)) in enumerate(shapes.items()):
+        r, K = dims[nm]
+        bt = (torch.randn(r, n, device=dev, generator=g) / n ** 0.5).to(torch.bfloat16)
+        a = (torch.randn(m, r, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
+        W[nm] = (bt, a)
+        aggs[nm] = pg.aggregate_layout(pg.FactorizedLayer.from_device(bt, a, K), [pats[j]], 0.9)
+        sel[nm] = torch.from_numpy(np.asarray(pats[j].indices, dtype=np.int64)).to(dev)
+
+    def ref(nm, x):  # f64 masked_forward on the bf16 weights
+        bt, a = W[nm]
+        s = sel[nm]
+        return a[:, s].double() @ (bt[s].double() @ x)
+
+    x = torch.randn(5120, device=dev, generator=g).to(torch.bfloat16)
+    xd = x.double()
+    ys = pg.module_forward([aggs[nm] for nm in ("q", "k", "v")], 0, x, out_dtype=torch.float32)
+    for nm, y in zip(("q", "k", "v"), ys):
+        want = ref(nm, xd)
+        assert float((y.double() - want).abs().max() / want.abs().max()) <= 1e-4, nm
+    y = pg.mlp_forward(aggs["up"], aggs["gate"], aggs["down"], 0, x, out_dtype=torch.float32)
+    u, gt = ref("up", xd), ref("gate", xd)
+    act = (gt * torch.sigmoid(gt) * u).to(torch.bfloat16).double()
+    want = ref("down", act)
+    assert float((y.double() - want).abs().max() / want.abs().max()) <= 2e-3
