@@ -948,8 +948,31 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
             torch.distributed.all_reduce(y)
 
     act = torch.empty(13824, device=dev, dtype=torch.bfloat16)
+    # --c5-peer 1 (world > 1): the decode token's all-reduces fused into the
+    # kernels over NVLink peer memory -- q, k, v, o through pg_agg_forward_peer,
+    # the MLP block through pg_mlp_forward_peer (one launch) -- no NCCL call
+    use_peer = bool(getattr(args, "c5_peer", 0)) and world > 1
+    if use_peer:
+        import ctypes as C
+        from paper_2605_08568_b200.api import _dtype_code, _ptr, call
+        grp = torch.distributed.group.WORLD
+        pbuf = {nm: pgd.PeerBuffer(LIN13[nm][0], world, rank, group=grp) for nm in ("q", "k", "v", "o")}
+        pbuf["mlp"] = pgd.PeerBuffer(2 * 13824 + 5120, world, rank, group=grp)
+        f32 = _dtype_code(torch.float32)
+        zeros3 = (C.c_size_t * 3)(0, 0, 0)
+
+    def decode_token_peer():
+        s = torch.cuda.current_stream(dev).cuda_stream
+        for nm in ("q", "k", "v", "o"):
+            call("pg_agg_forward_peer", lins[nm][0].handle, 0, _ptr(xd), _ptr(yd[nm]), f32, rank, world,
+                 pbuf[nm].ptrs, 0, s)
+        call("pg_mlp_forward_peer", lins["up"][0].handle, lins["gate"][0].handle, lins["down"][0].handle, zeros3,
+             _ptr(xd), _ptr(act), _ptr(yd["down"]), f32, rank, world, pbuf["mlp"].ptrs, 0, s)
 
     def decode_token():
+        if use_peer:
+            decode_token_peer()
+            return
         if world == 1:
             # one shard holds every expert: q/k/v as one fused module launch, o, and
             # the MLP block as one k_chain launch (up/gate -> silu -> down)
@@ -1025,8 +1048,12 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
                                 "frac": dec_bytes / (us_dec * 1e-6) / 1e9 / hbm_peak, "peak_kind": peak_kind},
             "prefill_flops_per_step": flops, "graph": bool(graphs),
             "decode_path": "world 1: q/k/v fused module + o + fused MLP block (k_chain), 3 launches per token"
-            if world == 1 else "per linear: aggregated_forward + NCCL all-reduce of the partial",
-            "collective": "torch.distributed.all_reduce (NCCL) of every linear's partial" if world > 1
+            if world == 1 else ("fused peer reduction: q, k, v, o (pg_agg_forward_peer) + the MLP block in one launch "
+                                "(pg_mlp_forward_peer), 5 launches per token, no NCCL" if use_peer else
+                                "per linear: aggregated_forward + NCCL all-reduce of the partial"),
+            "collective": ("decode: partials pushed as tagged words over NVLink peer memory (CUDA IPC), summed in "
+                           "rank order in-kernel; prefill: NCCL all-reduce" if use_peer else
+                           "torch.distributed.all_reduce (NCCL) of every linear's partial") if world > 1
             else "none (world 1: one shard holds every expert)"}
 
 
@@ -1073,6 +1100,8 @@ def main():
     ap.add_argument("--layers", type=int, default=N_LAYERS, help=argparse.SUPPRESS)
     ap.add_argument("--secondary", type=int, default=1, help="also run configs 1-3 (secondary objects)")
     ap.add_argument("--cpu", type=int, default=1, help="time the reference CPU path (rank 0, N=1)")
+    ap.add_argument("--c5-peer", type=int, default=0,
+                    help="config 5 at N > 1: decode all-reduces fused into the kernels over NVLink peer memory")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch plumbing only (no GPU): ranks, gloo process group, prompt partition, max-over-ranks")
     args = ap.parse_args()

@@ -288,6 +288,16 @@ int pg_union_prog_debug(pg_union_prog prog, uint64_t* out_host, size_t n, int* h
 int pg_peer_buffer_bytes(size_t m, size_t npeer, size_t* bytes);
 int pg_agg_forward_peer(pg_agg shard, size_t pattern, const void* x_dev, void* y_dev, pg_dtype y_dtype, int rank,
                         int npeer, void* const* peer_bufs, int grid, pg_stream stream);
+/* Expert-sharded MLP block (config 5 decode, toy_lm.hpp:250-257 with every
+ * linear sharded e mod npeer) in ONE launch: up/gate partials are pushed to
+ * every rank and summed in rank order per act row (so each rank forms the
+ * whole act = silu(gate) * up for its down shard), then down's partials are
+ * reduced the same way.  patterns[3] = local up/gate/down pattern ids; act
+ * (nullable) receives the reduced act; buffers: pg_peer_buffer_bytes(2 * m_ff
+ * + d, npeer) each, same rules as pg_agg_forward_peer. */
+int pg_mlp_forward_peer(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, const void* x_dev,
+                        void* act_dev, void* y_dev, pg_dtype y_dtype, int rank, int npeer, void* const* peer_bufs,
+                        int grid, pg_stream stream);
 int pg_ipc_get_handle(const void* dev_ptr, void* handle64_out);
 int pg_ipc_open_handle(const void* handle64, void** dev_ptr);
 int pg_ipc_close(void* dev_ptr);

@@ -81,6 +81,7 @@ _SIGS = {
     "pg_copy_io": [_vp, _vp, _sz, _vp],
     "pg_peer_buffer_bytes": [_sz, _sz, _vp],
     "pg_agg_forward_peer": [_vp, _sz, _vp, _vp, _i, _i, _i, _vp, _i, _vp],
+    "pg_mlp_forward_peer": [_vp, _vp, _vp, _sp, _vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp],
     "pg_ipc_get_handle": [_vp, _vp],
     "pg_ipc_open_handle": [_vp, _vp],
     "pg_ipc_close": [_vp],

@@ -759,6 +759,17 @@ static void run_chain_io(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& 
         P.npeer = peer->npeer;
         P.prank = peer->rank;
         for (int r = 0; r < peer->npeer; ++r) P.peer_recv[r] = static_cast<unsigned long long*>(peer->bufs[r]);
+        // words per (parity, rank): one linear's m rows, or an MLP block's up
+        // and gate rows (reduced into act mid-launch) followed by down's rows
+        if (mlp) {
+            if (phases.size() != 2) throw Error{PG_INVALID_ARGUMENT, "decode chain: peer MLP is one block"};
+            P.peer_words = 2 * phases[0][0].m + phases[1][0].m;
+            P.peer_last_off = 2 * phases[0][0].m;
+        } else {
+            if (phases.size() != 1) throw Error{PG_INVALID_ARGUMENT, "decode chain: peer launch is one linear"};
+            P.peer_words = phases[0][0].m;
+            P.peer_last_off = 0;
+        }
     }
     const size_t total = chain_tab_bytes(phases.size()) + xs_bytes + zs_bytes + kRingStages * (128 + 16) + 128 +
                          (size_t)kRingStages * ch;
@@ -1503,6 +1514,31 @@ int pg_agg_forward_peer(pg_agg g, size_t pattern, const void* x, void* y, pg_dty
     ps.grid = grid;
     ps.bufs = peer_bufs;
     run_chain(g->dt, ph, x, false, nullptr, ydt, as_stream(s), &ps);
+    PG_API_END
+}
+
+int pg_mlp_forward_peer(pg_agg up, pg_agg gate, pg_agg down, const size_t* patterns, const void* x, void* act,
+                        void* y, pg_dtype ydt, int rank, int npeer, void* const* peer_bufs, int grid, pg_stream s) {
+    PG_API_BEGIN
+    require(up && gate && down && patterns && x && y && peer_bufs && npeer >= 1 && npeer <= kMaxPeers && rank >= 0 &&
+                rank < npeer,
+            PG_INVALID_ARGUMENT, "mlp_forward_peer: bad arguments");
+    require(up->dt == gate->dt && up->dt == down->dt, PG_INVALID_ARGUMENT, "mlp_forward_peer: mixed dtypes");
+    require(up->dt != PG_F64 && ydt != PG_F64, PG_INVALID_ARGUMENT, "mlp_forward_peer: bf16/f32 layouts");
+    require(up->m == gate->m && up->n == gate->n && down->n == up->m, PG_INVALID_ARGUMENT,
+            "mlp_forward_peer: shape mismatch (up/gate m x n, down n x m)");
+    for (int r = 0; r < npeer; ++r) require(peer_bufs[r] != nullptr, PG_INVALID_ARGUMENT, "mlp_forward_peer: null buffer");
+    check_ydt(down->dt, ydt);
+    const std::vector<std::vector<LinSpec>> ph = {
+        {agg_spec(up, (int)patterns[0], nullptr, nullptr), agg_spec(gate, (int)patterns[1], nullptr, nullptr)},
+        {agg_spec(down, (int)patterns[2], nullptr, y)}};
+    require(chain_ok(up->dt, ph, true), PG_INVALID_ARGUMENT, "mlp_forward_peer: block too wide for the decode chain");
+    PeerSpec ps;
+    ps.rank = rank;
+    ps.npeer = npeer;
+    ps.grid = grid;
+    ps.bufs = peer_bufs;
+    run_chain(up->dt, ph, x, true, act, ydt, as_stream(s), &ps);
     PG_API_END
 }
 

@@ -56,6 +56,8 @@ struct ChainParams {
     int throttle;  // >= 0: after a stage-1 segment, at most this many chunks until the z exchange is done
     int l2hint;    // 1: weight copies carry an L2 evict-first policy
     int npeer, prank;
+    int peer_words;     // receive-buffer words per (parity, rank): m, or 2 m_ff + d for an MLP block
+    int peer_last_off;  // offset of the last phase's words (0, or 2 m_ff: up and gate come first)
     unsigned long long* peer_recv[kMaxPeers];
 };
 

@@ -714,7 +714,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                         }
                         a0 = warp_sum(a0);
                         a1 = warp_sum(a1);
-                        if (lane == 0) {
+                        if constexpr (PEER) {  // push the up/gate partials to every rank; act after the sum below
+                            if (lane < P.npeer) {
+                                unsigned long long* rb = P.peer_recv[lane] +
+                                                         ((size_t)(tag & 1u) * P.npeer + P.prank) * P.peer_words;
+                                xput(rb + i, __float_as_uint((float)a0), tag);
+                                xput(rb + L[0].m + i, __float_as_uint((float)a1), tag);
+                            }
+                        } else if (lane == 0) {
                             W* act = static_cast<W*>(Q.act);
                             if constexpr (sizeof(W) == 2) {
                                 const float up = (float)a0, g = (float)a1;
@@ -741,8 +748,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
                         acc = warp_sum(acc);
                         if constexpr (PEER) {  // push the partial to every rank (peer memory), reduce below
                             if (lane < P.npeer) {
-                                const int m = L[l].m;
-                                xput(P.peer_recv[lane] + ((size_t)(tag & 1u) * P.npeer + P.prank) * m + i,
+                                xput(P.peer_recv[lane] + ((size_t)(tag & 1u) * P.npeer + P.prank) * P.peer_words +
+                                         P.peer_last_off + i,
                                      __float_as_uint((float)acc), tag);
                             }
                         } else if (lane == 0) {
@@ -760,6 +767,29 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             if (last) break;
         }
         if (ph < 2) STAMP(ph * 6 + 5);
+        if constexpr (PEER) {
+            if (Q.epilogue == 1) {
+                // expert-sharded MLP block: this CTA's act rows from the ranks'
+                // up/gate partials, summed in rank order (identical on every
+                // rank), so every rank holds the whole act for its down shard
+                const int m0 = L[0].m;
+                const unsigned long long* mine = P.peer_recv[P.prank] + (size_t)(tag & 1u) * P.npeer * P.peer_words;
+                W* act = static_cast<W*>(Q.act);
+                for (int i = L[0].i0 + tid; i < L[0].i1; i += nct) {
+                    float u = 0.f, g = 0.f;
+                    for (int p = 0; p < P.npeer; ++p) {
+                        unsigned long long wu = xget(mine + (size_t)p * P.peer_words + i);
+                        unsigned long long wg = xget(mine + (size_t)p * P.peer_words + m0 + i);
+                        while ((uint32_t)(wu >> 32) != tag) wu = xget(mine + (size_t)p * P.peer_words + i);
+                        while ((uint32_t)(wg >> 32) != tag) wg = xget(mine + (size_t)p * P.peer_words + m0 + i);
+                        u += __uint_as_float((uint32_t)wu);
+                        g += __uint_as_float((uint32_t)wg);
+                    }
+                    if constexpr (sizeof(W) == 2) act[i] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+                    else act[i] = (W)(g / (1.0f + expf(-g)) * u);
+                }
+            }
+        }
         if (ph + 1 < P.nphase) grid_sync_consumers(P.bar);  // act complete before phase ph+1 reads it
     }
     if constexpr (PEER) {
@@ -767,17 +797,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
         // summed in rank order (deterministic on every rank)
         const LinS& Lr = lins[(P.nphase - 1) * kMaxLin];
         const uint32_t tag = *tag_s;
-        const int m = Lr.m;
-        const unsigned long long* mine = P.peer_recv[P.prank] + (size_t)(tag & 1u) * P.npeer * m;
+        const unsigned long long* mine =
+            P.peer_recv[P.prank] + (size_t)(tag & 1u) * P.npeer * P.peer_words + P.peer_last_off;
         for (int i = Lr.i0 + threadIdx.x; i < Lr.i1; i += kConsumerWarps * 32) {
             unsigned long long w[kMaxPeers];
 #pragma unroll
-            for (int p = 0; p < kMaxPeers; ++p) w[p] = p < P.npeer ? xget(mine + (size_t)p * m + i) : 0ull;
+            for (int p = 0; p < kMaxPeers; ++p) w[p] = p < P.npeer ? xget(mine + (size_t)p * P.peer_words + i) : 0ull;
             float v = 0.f;
 #pragma unroll
             for (int p = 0; p < kMaxPeers; ++p) {
                 if (p < P.npeer) {
-                    while ((uint32_t)(w[p] >> 32) != tag) w[p] = xget(mine + (size_t)p * m + i);
+                    while ((uint32_t)(w[p] >> 32) != tag) w[p] = xget(mine + (size_t)p * P.peer_words + i);
                     v += __uint_as_float((uint32_t)w[p]);
                 }
             }

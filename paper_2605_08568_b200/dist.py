@@ -212,27 +212,7 @@ class PeerReduceLinear:
 
     def prepare(self, sel):
         """Pack this rank's share of the selection (reused across decode steps)."""
-        from .api import RankSelection, aggregate_layout
-        if self._last is not None and self._last[0] is sel:  # decode steps reuse the same selection object
-            return self._last[1]
-        key = tuple(int(v) for v in np.asarray(sel.indices if hasattr(sel, "indices") else sel))
-        if key not in self._aggs:
-            mine = shard_selection(np.asarray(key, dtype=np.int64), self.world, self.rank)
-            if mine.size == 0:
-                # this rank owns none of the selected experts: it still launches
-                # (the other ranks wait for its pushes) and pushes exact zeros,
-                # through a one-expert all-zero layer of the same m x n
-                if self._zero is None:
-                    from .api import FactorizedLayer
-                    self._zero = FactorizedLayer(np.zeros((self.m, 1)), np.zeros((self.n, 1)), 1,
-                                                 dtype=self.local.dtype)
-                self._aggs[key] = aggregate_layout(self._zero, [RankSelection(np.zeros(1, dtype=np.uint32))],
-                                                   self.psi)
-            else:
-                self._aggs[key] = aggregate_layout(self.local, [RankSelection(self.shard.local_ids(mine))],
-                                                   self.psi)
-        self._last = (sel, self._aggs[key])
-        return self._aggs[key]
+        return _prepare_shard(self, sel)
 
     def forward(self, sel, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None) -> torch.Tensor:
         from .api import _TORCH, _dtype_code, _ptr, call
@@ -255,3 +235,126 @@ class PeerReduceLinear:
         for p in self._opened:
             call("pg_ipc_close", p)
         self._opened = []
+
+
+def _prepare_shard(h, sel):
+    """Aggregated layout of this rank's share S ∩ E_rank of a selection (cached
+    per selection; `h` carries shard / local / m / n / psi and the caches)."""
+    from .api import FactorizedLayer, RankSelection, aggregate_layout
+    if h._last is not None and h._last[0] is sel:  # decode steps reuse the same selection object
+        return h._last[1]
+    key = tuple(int(v) for v in np.asarray(sel.indices if hasattr(sel, "indices") else sel))
+    if key not in h._aggs:
+        mine = shard_selection(np.asarray(key, dtype=np.int64), h.world, h.rank)
+        if mine.size == 0:
+            # this rank owns none of the selected experts: it still launches
+            # (the other ranks wait for its pushes) and pushes exact zeros,
+            # through a one-expert all-zero layer of the same m x n
+            if h._zero is None:
+                h._zero = FactorizedLayer(np.zeros((h.m, 1)), np.zeros((h.n, 1)), 1, dtype=h.local.dtype)
+            h._aggs[key] = aggregate_layout(h._zero, [RankSelection(np.zeros(1, dtype=np.uint32))], h.psi)
+        else:
+            h._aggs[key] = aggregate_layout(h.local, [RankSelection(h.shard.local_ids(mine))], h.psi)
+    h._last = (sel, h._aggs[key])
+    return h._aggs[key]
+
+
+class _ShardHolder:
+    """One linear's expert shard inside PeerReduceMLP (see _prepare_shard)."""
+
+    def __init__(self, A, B, world, rank, dtype, psi):
+        from .api import FactorizedLayer
+        self.shard = shard_layer(np.asarray(A, dtype=np.float64), np.asarray(B, dtype=np.float64), world, rank)
+        self.world, self.rank, self.psi = world, rank, psi
+        self.m, self.n = self.shard.A.shape[0], self.shard.B.shape[0]
+        self.local = FactorizedLayer(self.shard.A, self.shard.B, None, dtype=dtype)
+        self._aggs, self._last, self._zero = {}, None, None
+
+
+class PeerReduceMLP(PeerReduceLinear):
+    """Expert-sharded MLP block (config 5 decode) in ONE decode-chain launch
+    per rank (pg_mlp_forward_peer): up and gate partials are pushed to every
+    rank's receive buffer and summed in rank order per act row, so every rank
+    forms the whole act = silu(gate) * up (toy_lm.hpp:250-257) for its down
+    shard; down's partials are then reduced the same way.  No NCCL call; the
+    result is identical on every rank.  `up`, `gate`, `down` are (A, B) factor
+    pairs (A m x r_store, B n x r_store); selections are global expert ids."""
+
+    def __init__(self, up, gate, down, world: int, rank: int, dtype="bf16", group=None, grid: int = 0,
+                 psi: float = 0.9):
+        from .api import call
+        if not 1 <= world <= 8:
+            raise ValueError("PeerReduceMLP: 1..8 ranks")
+        self.lins = [_ShardHolder(A, B, world, rank, dtype, psi) for A, B in (up, gate, down)]
+        u, g, d = self.lins
+        if u.m != g.m or u.n != g.n or d.n != u.m:
+            raise ValueError("PeerReduceMLP: shape mismatch (up/gate m x n, down n x m)")
+        self.world, self.rank, self.grid, self.psi = world, rank, grid, psi
+        self.m, self.n, self.m_ff = d.m, u.n, u.m
+        self.local = u.local
+        nb = C.c_size_t()
+        call("pg_peer_buffer_bytes", 2 * self.m_ff + self.m, world, C.byref(nb))
+        self.recv = torch.zeros(nb.value // 8, dtype=torch.int64, device="cuda")  # tags start at 1: zero = empty
+        self.peer_ptrs = None
+        self._opened = []
+        if group is not None and world > 1:
+            self._exchange(group)
+
+    @staticmethod
+    def local_group(up, gate, down, world: int, dtype="bf16", grid: int = 0) -> list:
+        """All ranks in this process (virtual ranks sharing one device)."""
+        ranks = [PeerReduceMLP(up, gate, down, world, r, dtype=dtype, grid=grid) for r in range(world)]
+        ptrs = [r.recv.data_ptr() for r in ranks]
+        for r in ranks:
+            r.peer_ptrs = ptrs
+        return ranks
+
+    def prepare(self, sels):
+        """Pack this rank's share of the (up, gate, down) selections."""
+        return [_prepare_shard(h, s) for h, s in zip(self.lins, sels)]
+
+    def forward(self, sels, x: torch.Tensor, out_dtype=torch.float32, out=None, act=None,
+                stream=None) -> torch.Tensor:
+        from .api import _TORCH, _dtype_code, _ptr, call
+        if self.peer_ptrs is None:
+            raise RuntimeError("PeerReduceMLP: receive buffers not exchanged")
+        aggs = self.prepare(sels)
+        x = x.reshape(-1)
+        if x.numel() != self.n:
+            raise ValueError("PeerReduceMLP: one token (x of n elements)")
+        x = x.to(self.local.torch_dtype).contiguous()
+        ydt = _dtype_code(out_dtype)
+        y = out if out is not None else torch.empty(self.m, dtype=_TORCH[ydt], device=x.device)
+        if act is not None and (act.numel() != self.m_ff or act.dtype != self.local.torch_dtype):
+            raise ValueError("PeerReduceMLP: act must hold m_ff elements of the weight dtype")
+        ptrs = (C.c_void_p * self.world)(*self.peer_ptrs)
+        pats = (C.c_size_t * 3)(0, 0, 0)
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        call("pg_mlp_forward_peer", aggs[0].handle, aggs[1].handle, aggs[2].handle, pats, _ptr(x),
+             _ptr(act) if act is not None else None, _ptr(y), ydt, self.rank, self.world, ptrs, self.grid, st)
+        return y
+
+
+class PeerBuffer:
+    """A zeroed receive buffer for the fused peer reductions
+    (pg_agg_forward_peer: words = m; pg_mlp_forward_peer: words = 2 m_ff + d)
+    with every rank's buffer pointer, exchanged as CUDA IPC handles over
+    `group` (one process per GPU).  `ptrs` is what the C-ABI takes."""
+
+    def __init__(self, words: int, world: int, rank: int, group=None):
+        from .api import call
+        nb = C.c_size_t()
+        call("pg_peer_buffer_bytes", words, world, C.byref(nb))
+        self.world, self.rank = world, rank
+        self.recv = torch.zeros(nb.value // 8, dtype=torch.int64, device="cuda")
+        self._opened = []
+        self.peer_ptrs = [self.recv.data_ptr()] if world == 1 else None
+        if group is not None and world > 1:
+            PeerReduceLinear._exchange(self, group)
+
+    @property
+    def ptrs(self):
+        return (C.c_void_p * self.world)(*self.peer_ptrs)
+
+    def close(self):
+        PeerReduceLinear.close(self)

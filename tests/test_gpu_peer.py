@@ -93,3 +93,46 @@ def test_peer_ipc_exchange_two_processes(tmp_path):
     for rank, rc, got in res:
         assert rc == 0
         assert got == [1000 + (rank - 1) % world] * 16
+
+
+@pytest.mark.parametrize("world,d,ff,dtype", [(2, 512, 1376, "bf16"), (4, 1024, 2752, "bf16"), (2, 512, 1376, "f32")])
+def test_peer_mlp_block_fused_allreduce(pg, port, world, d, ff, dtype):
+    """Expert-sharded MLP block in one launch per rank (pg_mlp_forward_peer):
+    up/gate partials reduced over the ranks into act mid-launch, then down's
+    partials; every rank ends with the same y, within the single-GPU MLP
+    tolerance of the f64 oracle composition on the same rounded inputs."""
+    from oracle import pyoracle
+    from paper_2605_08568_b200.dist import PeerReduceMLP
+    from tests.test_gpu_parity import _silu, bf16_round, make_layer_data
+    K = pg.single_layer_k(ff, d, 0.6)
+    r = pg.store_rank(K, d)
+    pats = pyoracle.make_patterns(17171 + world, 2, [(r, K)] * 3)
+    data = {nm: make_layer_data(port, *(shp + (r, 70 + i))) for i, (nm, shp) in
+            enumerate([("up", (ff, d)), ("gate", (ff, d)), ("down", (d, ff))])}
+    ranks = PeerReduceMLP.local_group(data["up"], data["gate"], data["down"], world, dtype=dtype, grid=148 // world)
+    streams = [torch.cuda.Stream() for _ in ranks]
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rnd = bf16_round if dtype == "bf16" else (lambda a: np.asarray(a, np.float32).astype(np.float64))
+    for step in range(4):  # repeated launches, alternating patterns: tag parity and per-selection packs
+        sels = [np.asarray(s, dtype=np.uint32) for s in pats[step % 2]]
+        for rk in ranks:
+            rk.prepare(sels)
+        x = port.gaussian(80 + step, (d, 1))
+        xd = torch.from_numpy(x[:, 0]).cuda().to(tdt)
+        torch.cuda.synchronize()
+        outs, acts = [], []
+        for rk, st in zip(ranks, streams):
+            with torch.cuda.stream(st):
+                a = torch.empty(ff, dtype=tdt, device="cuda")
+                outs.append(rk.forward(sels, xd, act=a, stream=st))
+                acts.append(a)
+        torch.cuda.synchronize()
+        for o, a in zip(outs[1:], acts[1:]):
+            assert torch.equal(o, outs[0]) and torch.equal(a, acts[0])
+        xr = rnd(x)
+        u = port.masked_forward(rnd(data["up"][0]), rnd(data["up"][1]), sels[0], xr)
+        g = port.masked_forward(rnd(data["gate"][0]), rnd(data["gate"][1]), sels[1], xr)
+        act = rnd(_silu(g) * u)
+        ref = port.masked_forward(rnd(data["down"][0]), rnd(data["down"][1]), sels[2], act)[:, 0]
+        y = outs[0].double().cpu().numpy()
+        assert np.abs(y - ref).max() / np.abs(ref).max() <= (2e-3 if dtype == "bf16" else 1e-5), step
