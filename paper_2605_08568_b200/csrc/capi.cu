@@ -728,12 +728,16 @@ static void run_chain_io(pg_dtype wdt, const std::vector<std::vector<LinSpec>>& 
     P.bar = reinterpret_cast<unsigned long long*>(base);
     P.epoch = reinterpret_cast<unsigned long long*>(base + 64);
     // measured: tagged z words win for the 2-phase MLP launch (30.5 vs 31.7 us
-    // per step), the fenced barrier for single-phase launches (13.6 vs 20.8 us)
+    // per step), the fenced barrier for single-linear launches (13.6 vs 20.8 us)
     static const int ztag_env = [] {
         const char* e = getenv("PG_CHAIN_ZTAG");
         return e ? atoi(e) : -1;
     }();
-    P.ztag = ztag_env >= 0 ? ztag_env : (mlp ? 1 : 0);
+    // and for single-phase modules of >= 2 linears (q/k/v, up/gate): 13B q/k/v
+    // 34.0 -> 30.0 us, 2-linear 25.6 -> 22.0; 7B q/k/v 20.5 -> 18.2, up/gate
+    // 24.3 -> 21.8 (tools/experiments/exp_c5_qkvo.py)
+    const bool multi = phases.size() == 1 && phases[0].size() >= 2;
+    P.ztag = ztag_env >= 0 ? ztag_env : ((mlp || multi) ? 1 : 0);
     size_t off = 256;
     for (size_t p = 0; p < phases.size(); ++p)
         if (act_off[p] != (size_t)-1) io.act[p] = base + zbytes + act_off[p];

@@ -678,11 +678,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) k_chain(const __grid_constan
             }
         }
         // ---- stage 2: y_i = A_S[i] . z
-        for (;;) {
+        for (int c2 = 0;; ++c2) {
             mbar_wait(smem_u32(&full[k]), (par >> k) & 1u);
             par ^= 1u << k;
             const Desc& D = descs[k];
             const int cnt = D.count, g0 = D.gidx, last = D.last, l = D.lin;
+            if (P.nphase == 1) {  // single-phase launches: stage-2 data arrival (first / last chunk)
+                if (c2 == 0) STAMP(7);
+                STAMP(8);
+            }
             if (cnt) {
                 const unsigned char* base = ring + (size_t)k * P.chunk_bytes;
                 for (int q = (warp - g0 % kConsumerWarps + kConsumerWarps) % kConsumerWarps; q < cnt;
