@@ -95,7 +95,8 @@ def test_peer_ipc_exchange_two_processes(tmp_path):
         assert got == [1000 + (rank - 1) % world] * 16
 
 
-@pytest.mark.parametrize("world,d,ff,dtype", [(2, 512, 1376, "bf16"), (4, 1024, 2752, "bf16"), (2, 512, 1376, "f32")])
+@pytest.mark.parametrize("world,d,ff,dtype", [(1, 512, 1376, "bf16"), (2, 512, 1376, "bf16"), (4, 1024, 2752, "bf16"),
+                                              (2, 512, 1376, "f32")])
 def test_peer_mlp_block_fused_allreduce(pg, port, world, d, ff, dtype):
     """Expert-sharded MLP block in one launch per rank (pg_mlp_forward_peer):
     up/gate partials reduced over the ranks into act mid-launch, then down's
