@@ -932,6 +932,8 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
         a = (torch.randn(m, cols, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
         mine = pgd.shard_selection(pats[j], world, rank)
         loc = (mine // world).astype(np.uint32) if mine.size else np.zeros(1, np.uint32)
+        if not mine.size:  # this rank owns none of the selected experts: it contributes an exact zero partial
+            bt, a = bt[:1].zero_(), a[:, :1].contiguous().zero_()
         L = pg.FactorizedLayer.from_device(bt, a, int(loc.size), layer_id=f"b0.{nm}")
         agg = pg.aggregate_layout(L, [pg.RankSelection(loc)], 0.9)
         lins[nm] = (agg, m, n, mine.size)
