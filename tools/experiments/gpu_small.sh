@@ -1,12 +1,10 @@
-O=gpurun_out; mkdir -p $O; : > $O/coop.txt
+O=gpurun_out; mkdir -p $O; : > $O/ctaep.txt
+timeout 600 python -m pytest tests -m gpu -x -q -k "chain or mlp or module or aggregated or decode or masked or peer or smoke" 2>&1 | tail -2 >> $O/ctaep.txt
 for i in 1 2; do
 for c in 1 0; do
-  echo "COOP=$c" >> $O/coop.txt
-  PG_CHAIN_COOP=$c EXP_ONLY=o EXP_SHAPE="256 256 0.6" timeout 120 python tools/experiments/exp_c5_qkvo.py >> $O/coop.txt 2>&1
-  PG_CHAIN_COOP=$c EXP_ONLY=o EXP_SHAPE="4096 4096 0.6" timeout 120 python tools/experiments/exp_c5_qkvo.py >> $O/coop.txt 2>&1
-  PG_CHAIN_COOP=$c EXP_SHAPE="5120 5120 0.4" timeout 120 python tools/experiments/exp_c5_qkvo.py >> $O/coop.txt 2>&1
-  PG_CHAIN_COOP=$c timeout 120 python tools/experiments/exp_c2_step.py >> $O/coop.txt 2>&1
+  PG_CHAIN_CTA_EPOCH=$c EXP_ONLY=o EXP_SHAPE="256 256 0.6" timeout 120 python tools/experiments/exp_c5_qkvo.py | sed "s/^/E$c /" >> $O/ctaep.txt 2>&1
+  PG_CHAIN_CTA_EPOCH=$c EXP_SHAPE="5120 5120 0.4" timeout 120 python tools/experiments/exp_c5_qkvo.py | sed "s/^/E$c /" >> $O/ctaep.txt 2>&1
+  PG_CHAIN_CTA_EPOCH=$c timeout 120 python tools/experiments/exp_c2_step.py | sed "s/^/E$c /" >> $O/ctaep.txt 2>&1
 done
 done
-PG_CHAIN_COOP=0 PG_CHAIN_DBG=1 EXP_ONLY=o EXP_SHAPE="256 256 0.6" timeout 120 python tools/experiments/exp_c5_qkvo.py 2>&1 | grep stamp >> $O/coop.txt
-cat $O/coop.txt
+cat $O/ctaep.txt
