@@ -82,6 +82,43 @@ def _body_sharded(rank, world):
     return rel, t, pgd.shard_selection(sel, world, rank).tolist(), [int(v) for v in sel]
 
 
+def _body_sharded_mlp(rank, world):
+    """The expert-sharded MLP block's algebra (PeerReduceMLP / pg_mlp_forward_peer):
+    up and gate partials summed over the ranks BEFORE the nonlinearity, every
+    rank forming the same act, then down's partials summed."""
+    from oracle import pyoracle
+    o = pyoracle.Oracle("port")
+    d, ff, r, K = 48, 112, 40, 17
+    fac = {nm: (o.gaussian(10 + i, (m, r)), o.gaussian(20 + i, (n, r)))
+           for i, (nm, m, n) in enumerate((("up", ff, d), ("gate", ff, d), ("down", d, ff)))}
+    sels = pyoracle.make_patterns(7, 1, [(r, K)] * 3)[0]
+    x = o.gaussian(30, (d, 1))
+
+    def fwd(sh, local_ids, xt):
+        y = o.masked_forward(sh.A, sh.B, np.asarray(local_ids, dtype=np.uint32), xt.numpy())
+        return torch.from_numpy(np.ascontiguousarray(y))
+
+    sh = {nm: pgd.shard_layer(A, B, world, rank) for nm, (A, B) in fac.items()}
+    u = pgd.sharded_forward(sh["up"], sels[0], torch.from_numpy(x), fwd).numpy()
+    g = pgd.sharded_forward(sh["gate"], sels[1], torch.from_numpy(x), fwd).numpy()
+    act = g / (1.0 + np.exp(-g)) * u
+    y = pgd.sharded_forward(sh["down"], sels[2], torch.from_numpy(act), fwd).numpy()
+    mf = lambda nm, s, v: o.masked_forward(fac[nm][0], fac[nm][1], np.asarray(s, dtype=np.uint32), v)  # noqa: E731
+    gu, gg = mf("up", sels[0], x), mf("gate", sels[1], x)
+    full = mf("down", sels[2], gg / (1.0 + np.exp(-gg)) * gu)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, act.tobytes())
+    return float(np.abs(y - full).max() / np.abs(full).max()), len(set(gathered))
+
+
+def test_expert_sharded_mlp_block_matches_single_process():
+    out = _run(_body_sharded_mlp)
+    for rank in (0, 1):
+        rel, distinct_acts = out[rank]
+        assert rel <= 1e-12, rel
+        assert distinct_acts == 1  # every rank holds the same act for its down shard
+
+
 def test_partitions_cover_and_agree():
     out = _run(_body_partitions)
     g0, g1 = out[0], out[1]
