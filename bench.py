@@ -941,7 +941,6 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
     xd = torch.randn(5120, device=dev, generator=g).to(torch.bfloat16)
     xpf = torch.randn(T_pre, 13824, device=dev, generator=g).to(torch.bfloat16)
     xdf = torch.randn(13824, device=dev, generator=g).to(torch.bfloat16)
-    yp = {nm: torch.empty(T_pre, m, device=dev) for nm, (_, m, _, _) in lins.items()}
     yd = {nm: torch.empty(m, device=dev) for nm, (_, m, _, _) in lins.items()}
     st = torch.cuda.Stream(device=dev)
 
@@ -988,11 +987,25 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
             pg.aggregated_forward(agg, 0, xdf if n == 13824 else xd, out_dtype=torch.float32, out=yd[nm])
             reduce(yd[nm])
 
+    # prefill chunk: linears that read the same hidden state run as one grouped
+    # tcgen05 launch per stage (q/k/v, then up/gate: the same x served by three /
+    # two layouts, x replicated per layout inside the step); o and down alone
+    groups = [("q", "k", "v"), ("o",), ("up", "gate"), ("down",)]
+    gx = {gr: torch.empty(len(gr) * T_pre, LIN13[gr[0]][1], device=dev, dtype=torch.bfloat16) for gr in groups}
+    gy = {gr: torch.empty(len(gr) * T_pre, LIN13[gr[0]][0], device=dev) for gr in groups}
+
     def step():
-        for nm, (agg, m, n, own) in lins.items():  # prefill chunk: T=256 tokens through each linear
+        for gr in groups:
+            n = LIN13[gr[0]][1]
             x = xpf if n == 13824 else xp
-            pg.aggregated_forward_batched(agg, [0], [0, T_pre], x, out_dtype=torch.float32, out=yp[nm])
-            reduce(yp[nm])
+            if len(gr) == 1:
+                pg.aggregated_forward_batched(lins[gr[0]][0], [0], [0, T_pre], x, out_dtype=torch.float32,
+                                              out=gy[gr])
+            else:
+                gx[gr].view(len(gr), T_pre, n).copy_(x.expand(len(gr), T_pre, n))
+                pg.prefill_batched([lins[nm][0] for nm in gr], [T_pre * i for i in range(len(gr) + 1)], gx[gr],
+                                   out_dtype=torch.float32, out=gy[gr])
+            reduce(gy[gr])
         for _ in range(n_dec):  # decode tokens reusing S
             decode_token()
 
@@ -1041,7 +1054,8 @@ def config5_arm(args, rank, world, local_rank, T_pre=256, n_dec=8, reps=10):
     flops = 2 * T_pre * sum(ldims[nm][1] * (m + n) for nm, (m, n) in LIN13.items())
     return {"workload": f"config5: LLaMA-13B decoder layer (q,k,v,o 5120x5120, gate/up 5120->13824, down "
                         f"13824->5120) ratio 0.4, expert-sharded over {world} GPU(s) (e mod G), per step 1 x "
-                        f"T={T_pre} prefill chunk + {n_dec} decode tokens through all 7 linears, partial outputs "
+                        f"T={T_pre} prefill chunk (q/k/v and up/gate grouped per stage) + {n_dec} decode tokens through all 7 "
+                        f"linears, partial outputs "
                         f"all-reduced (NCCL) per linear; bf16 weights, f32 outputs",
             "ms_per_step": ms, "tokens_per_s": (T_pre + n_dec) / (ms * 1e-3),
             "decode_us_per_token": us_dec, "decode_tokens_per_s": 1e6 / us_dec,
